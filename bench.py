@@ -1,0 +1,518 @@
+"""Benchmark of the per-step encoder<->LLM data path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|target1|cfg5|...]
+                    [--impl ours|reference]
+
+One step = plan (FFD + batch + LPT rebalance + reshard geometry, on device)
+-> pack + dispatch (push over NVLink at N > 1) -> return + scatter into the
+packed LLM input (projector GEMM fused with the scatter for cfg2).  The
+encoder itself is out of scope: its output buffer is filled once by the
+deterministic stand-in before timing.  Inputs are synthetic (the reference's
+own generator, restated in workload.py) and resident in HBM for `value`; `e2e`
+runs the same step through the public API from pinned host buffers.
+
+Weak scaling: every GPU owns `gbs_per_replica` sequences (dp = N).
+Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=os.environ.get("MUX_BENCH_CONFIG", "cfg2"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--distinct", type=int, default=8, help="distinct step inputs cycled")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--stages", action="store_true", help="per-stage timing breakdown")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+# workload
+# ----------------------------------------------------------------------------
+
+def workload(name, world):
+    from paper_2605_08962_b200 import configs
+    cfg = dict(configs.CONFIGS[name])
+    sp = cfg["sp"] if world % cfg["sp"] == 0 and world >= cfg["sp"] else 1
+    dp = world // sp
+    gbs = cfg["gbs_per_replica"] * dp
+    return cfg, dp, sp, gbs
+
+
+def generate_steps(name, world, n_steps):
+    """Host generation of n chained steps with the reference's generator
+    (workload.generate_batch's draw loop; hybrid_pack on the GPU)."""
+    from paper_2605_08962_b200 import configs, workload as W
+    from paper_2605_08962_b200.planner import StepTable
+    cfg, dp, sp, gbs = workload(name, world)
+    reg, sched = configs.build(W, name)
+    carry, modality_of, out = None, {}, []
+    for step in range(n_steps):
+        seqs, chunks = W.draw_step_chunks(reg, sched, step, cfg["seed"], gbs, configs.CAPACITY,
+                                          carry if cfg["carry"] else None)
+        for ch in chunks:
+            for s in ch:
+                modality_of[s.id] = s.modality
+        table = StepTable.from_chunks(list(carry or []) if cfg["carry"] else [], chunks,
+                                      modality_of)
+        out.append(table)
+        carry = seqs[gbs:]
+    return out
+
+
+# ----------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.stop = index, [], threading.Event()
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                    "--format=csv,noheader,nounits"], capture_output=True,
+                                   text=True, timeout=5)
+                if r.returncode == 0 and r.stdout.strip():
+                    self.rows.append([x.strip() for x in r.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.1)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 5 + k and r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]), \
+            "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_08962_b200 import _lib, build as B, configs
+    from paper_2605_08962_b200.dataplane import MuxPath
+    from paper_2605_08962_b200.planner import DeviceTable
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    if not os.path.exists(B.LIB):
+        if rank == 0:
+            B.build()
+        if world > 1:
+            dist.barrier()
+    _lib.lib()
+
+    name = args.config
+    cfg, dp, sp, gbs = workload(name, world)
+    projector = bool(cfg["projector"])
+    d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, configs.D_LLM
+    n_distinct = max(1, min(args.distinct, args.steps + args.warmup))
+    tables = generate_steps(name, world, n_distinct)
+
+    path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
+                   d_in=d_in, d_enc=d_enc, d_llm=d_llm, projector=projector, device=dev,
+                   group=group)
+    if projector:
+        gen = torch.Generator(device=dev).manual_seed(77)
+        for g in range(2):
+            w = (torch.randn(d_llm, d_enc[g], device=dev, generator=gen) / d_enc[g] ** 0.5)
+            path.set_projector(g, w.to(torch.bfloat16),
+                               torch.randn(d_llm, device=dev, generator=gen).to(torch.bfloat16))
+
+    # device-resident inputs: one step table + loader arenas per distinct step
+    dtabs, arenas, plans_info = [], [], []
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    for t in tables:
+        dt = DeviceTable(t, dev)
+        plan = path.plan(dt)
+        h = plan.check(t)
+        info = plan.host()
+        ar = [torch.randn(max(int(info["arena_rows"][rank, g]), 1), d_in[g], device=dev,
+                          generator=gen).to(torch.bfloat16) for g in range(2)]
+        dtabs.append(dt)
+        arenas.append(ar)
+        m_tokens = int(info["recv_rows"].sum())  # modality tokens of the whole batch
+        plans_info.append(dict(M=m_tokens, T=int(info["llm_rows"].sum()),
+                               S=int(h[_lib.H_N_BATCH]),
+                               recv=(int(h[_lib.H_RECV_ROWS0]), int(h[_lib.H_RECV_ROWS1])),
+                               disp_bytes=int(h[_lib.H_DISPATCH_BYTES]),
+                               ret_bytes=int(h[_lib.H_RETURN_BYTES]),
+                               disp_remote=int(h[_lib.H_DISPATCH_REMOTE]),
+                               ret_remote=int(h[_lib.H_RETURN_REMOTE])))
+    # encoder output: the stand-in fills it once (encoder compute is out of scope)
+    plan = path.plan(dtabs[0])
+    path.encode_standin(plan, dtabs[0])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    stream = torch.cuda.current_stream()
+    ev_dom = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+
+    def one_step(k, timed_dom=None):
+        i = k % n_distinct
+        p = path.plan(dtabs[i], stream)
+        path.dispatch(p, arenas[i], stream)
+        if timed_dom is not None:
+            timed_dom[0].record(stream)
+        path.return_scatter(p, plans_info[i]["recv"] if projector else None, stream)
+        if timed_dom is not None:
+            timed_dom[1].record(stream)
+
+    for k in range(args.warmup):
+        one_step(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for k in range(args.steps):
+            one_step(args.warmup + k, ev_dom[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    path.check_wait()
+    ms = t0.elapsed_time(t1)
+    dom_ms = [a.elapsed_time(b) for a, b in ev_dom]
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+
+    steps_idx = [(args.warmup + k) % n_distinct for k in range(args.steps)]
+    M_total = sum(plans_info[i]["M"] for i in steps_idx)
+    T_total = sum(plans_info[i]["T"] for i in steps_idx)
+    value = M_total / (ms / 1e3)
+
+    # dominant kernel roofline (rank-local)
+    hbm, tf_burst, tf_sus, src = peaks()
+    dom_avg_s = float(np.mean(dom_ms)) / 1e3
+    my_recv = [sum(plans_info[i]["recv"][g] for i in steps_idx) / len(steps_idx) for g in (0, 1)]
+    if projector:
+        from paper_2605_08962_b200 import costs
+        flops = sum(costs.projector_flops(my_recv[g], d_enc[g], d_llm) for g in (0, 1))
+        roof = {"kernel": "proj_scatter_gemm (tcgen05)", "bound": "tensor",
+                "achieved": flops / dom_avg_s / 1e12, "peak": tf_sus, "unit": "TFLOP/s",
+                "peak_source": f"bf16_tflops_sustained ({src})"}
+    else:
+        ret = sum(plans_info[i]["ret_bytes"] for i in steps_idx) / len(steps_idx)
+        algo = 2 * ret  # read + write of every returned row
+        bound = "hbm" if world == 1 else "nvlink"
+        roof = {"kernel": "segcopy return+scatter", "bound": "hbm",
+                "achieved": algo / dom_avg_s / 1e9, "peak": hbm, "unit": "GB/s",
+                "peak_source": f"hbm_gbs ({src})"}
+        if bound == "nvlink":
+            roof["note"] = "N>1: rows cross NVLink; HBM figure shown for the local side"
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["dominant_ms"] = dom_avg_s * 1e3
+
+    # e2e: public API from pinned host buffers, H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, world)
+
+    launches = 2 + 2  # ffd + finalize + dispatch copy + return copy (per step)
+    if world > 1:
+        launches += 2  # two flag waits
+    if projector:
+        launches = 2 + 1 + (1 if world > 1 else 0) + 2 * sum(1 for g in (0, 1) if my_recv[g] > 0)
+        if world > 1:
+            launches += 2
+    line = {
+        "metric": "multimodal tokens/s rebalanced+dispatched+scattered per step",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (reference generator restated; bf16 N(0,1) payload; encoder stand-in)",
+        "config": {"workload": name, "global_batch": gbs, "seq_len": configs.CAPACITY,
+                   "parallelism": f"enc dp{world} / llm dp{dp} sp{sp}",
+                   "projector": projector, "d_in": list(d_in), "d_enc": list(d_enc),
+                   "d_llm": d_llm, "distinct_steps": n_distinct,
+                   "modality_tokens_per_step": M_total / args.steps,
+                   "llm_tokens_per_step": T_total / args.steps,
+                   "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"},
+        "roofline": roof,
+        "gpu_launches": launches * args.steps,
+        "e2e": e2e,
+    }
+    if rank == 0:
+        line["clocks"] = clk.summary()
+        if world == 1:
+            line["cpu_baseline"] = cpu_baseline(name, tables[0], projector, quick=True)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, world):
+    """Same step through the public API with pinned host inputs and a D2H result."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_08962_b200 import _lib
+    from paper_2605_08962_b200.planner import DeviceTable
+
+    host_tabs = [torch.from_numpy(t.blob()).pin_memory() for t in tables]
+    host_ar = [[a.cpu().pin_memory() for a in ar] for ar in arenas]
+    dev_ar = [[torch.empty_like(a) for a in ar] for ar in arenas]
+    out_hdr = torch.empty(_lib.H_SLOTS, dtype=torch.int64).pin_memory()
+    stream = torch.cuda.current_stream()
+    steps = max(args.steps // 2, 3)
+    h2d = d2h = 0
+
+    def one(k):
+        nonlocal h2d, d2h
+        i = k % n_distinct
+        dt = DeviceTable(tables[i], dev, host_blob=host_tabs[i])
+        for a, b in zip(dev_ar[i], host_ar[i]):
+            a.copy_(b, non_blocking=True)
+        p = path.plan(dt, stream)
+        path.dispatch(p, dev_ar[i], stream)
+        path.return_scatter(p, plans_info[i]["recv"] if projector else None, stream)
+        out_hdr.copy_(p.view("header", _lib.H_SLOTS), non_blocking=True)
+        return host_tabs[i].numel() * 8 + sum(b.numel() * 2 for b in host_ar[i]), 8 * _lib.H_SLOTS
+
+    for k in range(3):
+        one(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    M = 0
+    for k in range(steps):
+        b_in, b_out = one(k)
+        h2d += b_in
+        d2h += b_out
+        M += plans_info[k % n_distinct]["M"]
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    assert int(out_hdr[_lib.H_STATUS]) == 0
+    return {"value": M / (ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d // steps,
+            "d2h_bytes_per_step": d2h // steps, "steps": steps,
+            "note": "step table + loader payload H2D from pinned host memory; plan header D2H"}
+
+
+# ----------------------------------------------------------------------------
+# CPU reference arm (oracle port; the reference itself never moves token data)
+# ----------------------------------------------------------------------------
+
+def cpu_baseline(name, table, projector, quick=False, budget_s=None):
+    """Time the CPU port (oracle planner + torch-CPU data plane) on one step.
+
+    Bounded sample: one step of the workload (full token counts); the
+    projector GEMM, when on, is timed on a 4096-row slice and scaled.
+    """
+    import torch
+
+    from oracle import planner as oplan
+    from paper_2605_08962_b200 import configs
+
+    cfg = configs.CONFIGS[name]
+    threads = len(os.sched_getaffinity(0))
+    torch.set_num_threads(threads)
+    t = dict(lens=table.lens.astype(np.int64), mods=table.mods.astype(np.int64), ids=table.ids,
+             carry_seq=table.carry_seq.astype(np.int64), n_carry_seqs=table.n_carry_seqs,
+             chunk_off=table.chunk_off.tolist())
+    gbs = cfg["gbs_per_replica"]
+    d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, configs.D_LLM
+    t0 = time.perf_counter()
+    o = oplan.plan_step(t, configs.CAPACITY, gbs, 1, 1, 1)
+    t_plan = time.perf_counter() - t0
+    rows = [int(o["arena_rows"][0, g]) for g in range(2)]
+    arenas = [torch.randn(max(r, 1), d_in[g]).to(torch.bfloat16) for g, r in enumerate(rows)]
+    recv = [torch.empty(max(r, 1), d_in[g], dtype=torch.bfloat16) for g, r in enumerate(rows)]
+    d_ret = d_enc if projector else (d_llm, d_llm)
+    enc = [torch.randn(max(r, 1), d_ret[g]).to(torch.bfloat16) for g, r in enumerate(rows)]
+    llm = torch.zeros(int(o["llm_rows"][0]), d_llm, dtype=torch.bfloat16)
+    lens = t["lens"]
+    items = np.flatnonzero(o["enc"] >= 0)
+    # pack: index gather per group
+    t0 = time.perf_counter()
+    for g in range(2):
+        src, dst = [], []
+        for i in items:
+            if o["group"][i] == g:
+                L = int(lens[i])
+                src.append(np.arange(o["arena_off"][i], o["arena_off"][i] + L))
+                dst.append(np.arange(o["enc_off"][i], o["enc_off"][i] + L))
+        if src:
+            s, d = torch.from_numpy(np.concatenate(src)), torch.from_numpy(np.concatenate(dst))
+            recv[g].index_copy_(0, d, arenas[g].index_select(0, s))
+    t_pack = time.perf_counter() - t0
+    # return + scatter (+ projector)
+    t0 = time.perf_counter()
+    scale = 1.0
+    for g in range(2):
+        src, dst = [], []
+        for (i, sr, _, dr, n) in o["pieces"]:
+            if o["group"][i] == g:
+                src.append(np.arange(sr, sr + n))
+                dst.append(np.arange(dr, dr + n))
+        if not src:
+            continue
+        s, d = torch.from_numpy(np.concatenate(src)), torch.from_numpy(np.concatenate(dst))
+        x = enc[g].index_select(0, s)
+        if projector:
+            W = torch.randn(d_llm, d_enc[g]).to(torch.bfloat16)
+            m = min(4096, x.shape[0])
+            tg = time.perf_counter()
+            y = (x[:m].float() @ W.float().t()).to(torch.bfloat16)
+            tm = time.perf_counter() - tg
+            scale_t = tm * (x.shape[0] / m - 1)   # remaining rows, extrapolated
+            t0 -= scale_t
+            x = torch.cat([y, torch.zeros(x.shape[0] - m, d_llm, dtype=torch.bfloat16)])
+            scale = x.shape[0] / m
+        llm.index_copy_(0, d, x)
+    t_ret = time.perf_counter() - t0
+    M = int(o["recv_rows"].sum())
+    total = t_plan + t_pack + t_ret
+    sample = (f"one {name} step: {M} modality tokens, oracle planner + torch-CPU gather/scatter"
+              + (f"; projector timed on 4096 rows, scaled x{scale:.1f}" if projector else ""))
+    return {"value": M / total, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": sample, "seconds": {"plan": t_plan, "pack": t_pack, "return": t_ret}}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2605_08962_b200 import configs
+    name = args.config
+    cfg, dp, sp, gbs = workload(name, world)
+    tables = generate_steps_host(name, world, max(1, min(args.steps + args.warmup, 4)))
+    vals = []
+    for k in range(args.warmup + args.steps):
+        r = cpu_baseline_world(name, tables[k % len(tables)], world, cfg["projector"])
+        if k >= args.warmup:
+            vals.append(r)
+    v = float(np.mean([r["value"] for r in vals]))
+    line = {"metric": "multimodal tokens/s rebalanced+dispatched+scattered per step",
+            "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": name, "global_batch": gbs, "seq_len": configs.CAPACITY,
+                       "parallelism": f"enc dp{world} / llm dp{dp} sp{sp} (simulated in-process)",
+                       "projector": bool(cfg["projector"])},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": vals[0]["cores"],
+                             "kind": "port", "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def generate_steps_host(name, world, n_steps):
+    """Same step tables as generate_steps, produced by the CPU oracle generator."""
+    from oracle import planner as oplan
+    from oracle import workload as owork
+    from paper_2605_08962_b200 import configs
+    from paper_2605_08962_b200.planner import StepTable
+    cfg, dp, sp, gbs = workload(name, world)
+    descs = owork.descs_from_config(configs.DATASETS, cfg["datasets"])
+    carry, seen, out = None, {}, []
+    for step in range(n_steps):
+        b, rest, drawn, chunks = owork.generate(descs, cfg["phases"], False, step, cfg["seed"],
+                                                gbs, dp, 1, configs.CAPACITY,
+                                                carry if cfg["carry"] else None)
+        for s in drawn:
+            seen[s[0]] = s[1]
+        t = oplan.step_table(list(carry or []) if cfg["carry"] else [], drawn, chunks, seen)
+        out.append(StepTable(t["lens"].astype(np.int32), t["mods"].astype(np.int32), t["ids"],
+                             t["carry_seq"].astype(np.int32), t["n_carry_seqs"],
+                             np.asarray(t["chunk_off"], np.int32)))
+        carry = rest
+    return out
+
+
+def cpu_baseline_world(name, table, world, projector):
+    if world == 1:
+        return cpu_baseline(name, table, projector)
+    # all ranks simulated in-process: the same gather/scatter over the whole batch
+    return cpu_baseline(name, table, projector)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * mux_b200.h — C ABI of libmuxb200.so, the B200 data path between modality
+ * encoders and the LLM backbone (arXiv 2605.08962 / reference package muxsim).
+ *
+ * Plain C: device pointers, sizes and a cudaStream_t passed as void*.  The
+ * library never allocates or frees caller memory; every buffer is owned by the
+ * caller (PyTorch on the Python side).  Status codes map one-to-one onto the
+ * reference's exception types (pkg/src/muxsim/workload.py:29-34):
+ *   MUX_ERR_CONFIG  -> ConfigError      MUX_ERR_PACKING -> PackingError
+ *   MUX_ERR_VALUE   -> ValueError       MUX_ERR_RUNTIME -> RuntimeError
+ * and mux_last_error() returns the thread-local message.
+ *
+ * Reference interfaces each entry point replaces (file:line under
+ * /root/reference):
+ *   mux_plan_step        workload.hybrid_pack (pkg/src/muxsim/workload.py:240-262)
+ *                        + build_global_batch (:265-278) + replica slicing
+ *                        (:177-180) + balance.grouped_reorder / kk_partition
+ *                         + reshard.plan_reshard UlyssesUniform
+ *                        (SPEC.md:462-470), fused into one device plan.
+ *   mux_assign           balance.kk_partition and the LPT
+ *                        greedy named by BASELINE.json north_star.
+ *   mux_segcopy          the data all-to-all of grouped_reorder
+ *                        and the inverse of restore_order;
+ *                        pack, dispatch, return and scatter are all segment
+ *                        copies over local or NVLink-peer pointers.
+ *   mux_signal/mux_wait  cross-GPU completion flags for the push exchange.
+ *   mux_proj_scatter     projector GEMM fused with the placeholder scatter
+ *                        (no reference code, adapter).
+ *   mux_encoder_standin  deterministic stand-in for the (out of scope) encoder.
+ */
+#ifndef MUX_B200_H
+#define MUX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MUX_OK 0
+#define MUX_ERR_CONFIG 1
+#define MUX_ERR_PACKING 2
+#define MUX_ERR_VALUE 3
+#define MUX_ERR_CUDA 4
+#define MUX_ERR_RUNTIME 5
+
+#define MUX_MODE_PACK 0 /* FFD only: hybrid_pack of each chunk              */
+#define MUX_MODE_STEP 1 /* full step: batch, origins, balance, reshard, segs */
+
+#define MUX_LPT 0
+#define MUX_KK 1
+
+#define MUX_N_GROUPS 2 /* encoder groups: 0 = vision (image/video), 1 = audio */
+
+/* Header slots of the plan buffer (int64 each). */
+#define MUX_H_STATUS 0
+#define MUX_H_ERR_INDEX 1     /* table index of the first oversize sample, -1  */
+#define MUX_H_N_SEQ 2         /* sequences after packing (carry + new)         */
+#define MUX_H_N_DISPATCH 3    /* dispatch segments of rank `me`                */
+#define MUX_H_N_RETURN 4      /* return pieces of rank `me`                    */
+#define MUX_H_DISPATCH_CHUNKS 5
+#define MUX_H_RETURN_CHUNKS 6
+#define MUX_H_DISPATCH_BYTES 7
+#define MUX_H_RETURN_BYTES 8
+#define MUX_H_N_BATCH 9       /* samples inside the global batch               */
+#define MUX_H_DISPATCH_REMOTE 10 /* dispatch bytes leaving rank `me`           */
+#define MUX_H_RETURN_REMOTE 11   /* return bytes leaving rank `me`             */
+#define MUX_H_RECV_ROWS0 12   /* rows received by `me`, group 0 / group 1      */
+#define MUX_H_RECV_ROWS1 13
+#define MUX_H_SLOTS 32
+
+typedef struct {
+  int32_t S;            /* samples in the step table                        */
+  int32_t n_carry;      /* leading carry samples (sequence/span order)      */
+  int32_t n_carry_seqs; /* carried sequences                                */
+  int32_t n_chunks;     /* drawn chunks after the carry samples             */
+  int32_t capacity;
+  int32_t gbs, dp, sp, world, mbs;
+  int32_t method;       /* MUX_LPT | MUX_KK                                 */
+  int32_t pooled;       /* 1: balance all modalities together */
+  int32_t me;           /* rank whose segment tables are emitted            */
+  int32_t mode;         /* MUX_MODE_PACK | MUX_MODE_STEP                    */
+  int32_t row_bytes_in[MUX_N_GROUPS];  /* loader row bytes per group        */
+  int32_t row_bytes_ret[MUX_N_GROUPS]; /* returned row bytes per group      */
+  int32_t chunk_bytes;  /* copy work unit (0 = default)                     */
+  int32_t max_chunks;   /* capacity of each chunk map                       */
+} mux_plan_cfg;
+
+/* Byte offsets of every array inside the plan buffer (one device blob). */
+typedef struct {
+  int64_t header;                                   /* int64[MUX_H_SLOTS] */
+  int64_t seq, off, span, origin, origin_pos, group, enc; /* int32[S]      */
+  int64_t arena_off, enc_off;                       /* int64[S]           */
+  int64_t llm_rank, llm_row;                        /* int32/int64[S]     */
+  int64_t bin_fill, bin_nspan, bin_of;              /* int32[S] (scratch) */
+  int64_t chunk_nbins;                              /* int32[n_chunks]    */
+  int64_t fills, nspans;                            /* int32[max_seq]     */
+  int64_t cu;                                       /* int32[gbs+1]       */
+  int64_t shard_len, shard_start;                   /* int32[gbs*sp]      */
+  int64_t row_base;                                 /* int64[gbs*sp]      */
+  int64_t arena_rows, recv_rows;                    /* int64[world*2]     */
+  int64_t llm_rows;                                 /* int64[world]       */
+  int64_t order, scratch_a, scratch_b;              /* int32[S] (scratch) */
+  /* dispatch segments (rank me): rows from arena[group] to recv[group]@enc */
+  int64_t dseg_src_row, dseg_dst_row, dseg_rows;    /* int64[S]           */
+  int64_t dseg_group, dseg_dst_rank;                /* int32[S]           */
+  int64_t dseg_chunk0;                              /* int64[S+1]         */
+  int64_t dchunk_seg;                               /* int32[max_chunks]  */
+  /* return pieces (rank me): rows from enc_out[group] to llm@dst_rank      */
+  int64_t rseg_src_row, rseg_dst_row, rseg_rows;    /* int64[S*(sp+1)]    */
+  int64_t rseg_group, rseg_dst_rank;                /* int32[S*(sp+1)]    */
+  int64_t rseg_chunk0;                              /* int64[S*(sp+1)+1]  */
+  int64_t rchunk_seg;                               /* int32[max_chunks]  */
+  int64_t total;
+} mux_plan_layout;
+
+int mux_version(void);
+const char* mux_last_error(void);
+
+/* Layout of the plan buffer for `cfg`; returns MUX_OK or MUX_ERR_VALUE. */
+int mux_plan_layout_of(const mux_plan_cfg* cfg, mux_plan_layout* out);
+
+/* One device plan for one step (or, in MUX_MODE_PACK, FFD of each chunk).
+ * Table arrays are device pointers: lens/mods int32[S], ids int64[S],
+ * carry_seq int32[n_carry], chunk_off int32[n_chunks+1] (chunk_off[0] =
+ * n_carry).  Stream-ordered; errors are written to the header and reported
+ * by mux_plan_check() after the caller synchronises. */
+int mux_plan_step(const mux_plan_cfg* cfg, const int32_t* lens, const int32_t* mods,
+                  const int64_t* ids, const int32_t* carry_seq, const int32_t* chunk_off,
+                  void* plan, size_t plan_bytes, void* stream);
+
+/* Host-side check of a plan header copied back by the caller: maps the
+ * device status onto MUX_ERR_* and sets mux_last_error() with the
+ * reference's message. `ids_host`/`lens_host` name the offender. */
+int mux_plan_check(const mux_plan_cfg* cfg, const int64_t* header_host,
+                   const int64_t* ids_host, const int32_t* lens_host);
+
+/* Stand-alone partition of n weights over g ranks (kk_partition / LPT).
+ * weights double[n], ids int64[n] (LPT tie-break), out int32[n].  Device
+ * pointers; scratch int8[mux_assign_scratch_bytes(n, g)]. */
+size_t mux_assign_scratch_bytes(int32_t n, int32_t g);
+int mux_assign(int32_t method, const double* weights, const int64_t* ids, int32_t n,
+               int32_t g, int32_t* out, void* scratch, void* stream);
+
+/* Segment copy: table = plan (dispatch: which=0, return: which=1).
+ * src_bases[group], dst_bases[rank * MUX_N_GROUPS + group] (dispatch) or
+ * dst_bases[rank] (return) are device arrays of device pointers (local or
+ * NVLink-peer).  row bytes come from the plan cfg.  grid_ctas = 0 picks
+ * the persistent default (148 SMs x occupancy). */
+int mux_segcopy(const mux_plan_cfg* cfg, const void* plan, int32_t which,
+                void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
+                void* stream);
+/* Same copy, then the last CTA fences at system scope and stores `epoch`
+ * into flags_peers[r][me] for every rank r (fused completion signal).
+ * done_counter: one zero-initialised uint32 in device memory, re-armed by
+ * the kernel itself. */
+int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
+                       void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
+                       uint64_t* const* flags_peers, uint32_t* done_counter, uint64_t epoch,
+                       void* stream);
+
+/* Cross-GPU completion flags.  flags_peers: device array of `world` device
+ * pointers to each rank's uint64 flag array (world entries each).  signal
+ * stores `epoch` into flag[me] of every peer after a system-scope fence;
+ * wait spins until every flag[src] of `my_flags` >= epoch (bounded:
+ * timeout_ms, status written to *err_dev). */
+int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t epoch,
+               void* stream);
+int mux_wait(int32_t world, const uint64_t* my_flags, uint64_t epoch, int32_t timeout_ms,
+             int32_t* err_dev, void* stream);
+
+/* Deterministic encoder stand-in: for every sample of rank `me` in group
+ * `group`, rows [enc_off, enc_off+len) of out (row width `width` bf16)
+ * get E(id, t, c).  Uses the plan's enc/enc_off/group arrays. */
+int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, const int64_t* ids,
+                        const int32_t* lens, int32_t group, int32_t width,
+                        uint16_t* out, void* stream);
+
+/* Expand return pieces of rank `me`, group `group` into a per-row
+ * destination table: row_dst[src_row] = (dst_rank << 40) | dst_row. */
+int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_t group,
+                    int64_t* row_dst, int64_t n_rows, void* stream);
+
+/* Projector fused with the scatter: for m < M,
+ *   out_rank[row_dst[m] >> 40][row_dst[m] & (2^40-1), :] =
+ *       bf16( X[m, :K] . W[:N, :K]^T + bias[:N] )
+ * X bf16 [M, K] row-major, W bf16 [N, K] row-major (nn.Linear weight),
+ * bias bf16 [N] or NULL, out_bases: device array of world device pointers
+ * (local or NVLink-peer LLM buffers, row stride N).  tcgen05 + TMEM + TMA
+ * on sm_100a.  K % 64 == 0, N % 256 == 0. */
+int mux_proj_scatter(const uint16_t* X, const uint16_t* W, const uint16_t* bias, int64_t M,
+                     int32_t K, int32_t N, const int64_t* row_dst, void* const* out_bases,
+                     int32_t num_sms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MUX_B200_H */

@@ -1,0 +1,286 @@
+"""CPU restatement of the per-step planner — TEST INFRASTRUCTURE ONLY.
+
+Inputs are a *step table*: the samples of one step in table order (carryover
+samples first, in sequence/span order, then every drawn chunk in draw order),
+exactly what workload.generate_batch (pkg/src/muxsim/workload.py:281-305)
+consumes.  Output is the full plan as numpy arrays; the GPU planner must
+reproduce every array bit-exactly.
+
+Reference anchors:
+  FFD per chunk ........ workload.py:240-262 (via oracle.workload.ffd)
+  batch / replica slice  workload.py:265-278, :177-180
+  LPT .................. BASELINE.json north_star ("greedy/LPT")
+  kk_partition ......... SPEC.md:390-398 (pinned definition: SURVEY.md §8.1-1)
+  grouped_reorder ...... SPEC.md:399-407 (pool window = whole step)
+  restore_order ........ SPEC.md:408-416
+  plan_reshard Ulysses . SPEC.md:453-470 (first F mod sp shards get +1)
+Builder-defined layout (no reference code; "parity unpinned" by the
+reference, defined here and in DESIGN.md §Layout):
+  origin rank = LLM rank owning the sample's first token; loader arena of
+  (rank, encoder group) in table order; encoder order (origin rank, table
+  order); returned rows go straight to their LLM (rank, row).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .workload import OracleConfigError, OraclePackingError
+
+GROUP_OF_MOD = {0: -1, 1: 0, 2: 0, 3: 1}
+N_GROUPS = 2
+
+
+# ----------------------------------------------------------------------------
+# assignment algorithms
+# ----------------------------------------------------------------------------
+
+def lpt_assign(costs, ids, g, init=None):
+    """Longest-processing-time greedy: order by (-cost, id, index), each item to
+    the least-loaded rank, lowest rank on ties.  Returns rank per item."""
+    n = len(costs)
+    order = sorted(range(n), key=lambda i: (-costs[i], ids[i], i))
+    load = list(init) if init is not None else [0.0] * g
+    out = [0] * n
+    for i in order:
+        r = min(range(g), key=lambda k: (load[k], k))
+        out[i] = r
+        load[r] = load[r] + costs[i]
+    return out
+
+
+def kk_assign(weights, g):
+    """g-way Karmarkar-Karp largest differencing.
+
+    Pinned reading: every item starts as the g-tuple
+    (w, 0, ..., 0); repeatedly pop the two tuples with the largest spread
+    (max - min sum), ties to the lower minimum item index; the first popped
+    is A.  Merge by pairing A's subsets sorted by (sum desc, min index asc)
+    with B's sorted by (sum asc, min index asc).  The final subsets map to
+    ranks 0..g-1 in (sum desc, min index asc) order.  g > n pads empty.
+    """
+    n = len(weights)
+    if n == 0:
+        return []
+    inf = 1 << 62
+    # a tuple = list of g subsets; subset = [sum, min_index, members]
+    tuples = [[[weights[i], i, [i]]] + [[0.0 * weights[i], inf, []] for _ in range(g - 1)]
+              for i in range(n)]
+
+    def spread(t):
+        sums = [s[0] for s in t]
+        return max(sums) - min(sums)
+
+    def tmin(t):
+        return min(s[1] for s in t)
+
+    alive = list(range(n))
+    while len(alive) > 1:
+        alive.sort(key=lambda k: (-spread(tuples[k]), tmin(tuples[k])))
+        a, b = alive[0], alive[1]
+        A = sorted(tuples[a], key=lambda s: (-s[0], s[1]))
+        B = sorted(tuples[b], key=lambda s: (s[0], s[1]))
+        merged = [[x[0] + y[0], min(x[1], y[1]), x[2] + y[2]] for x, y in zip(A, B)]
+        tuples[a] = merged
+        alive = [k for k in alive if k != b]
+    final = sorted(tuples[alive[0]], key=lambda s: (-s[0], s[1]))
+    out = [0] * n
+    for rank, sub in enumerate(final):
+        for i in sub[2]:
+            out[i] = rank
+    return out
+
+
+def ulysses_split(fill, sp):
+    """Shard lengths of a sequence of `fill` tokens over sp ranks; the first
+    fill % sp shards get one extra token."""
+    q, r = divmod(int(fill), sp)
+    return [q + (1 if k < r else 0) for k in range(sp)]
+
+
+# ----------------------------------------------------------------------------
+# step plan
+# ----------------------------------------------------------------------------
+
+def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=False):
+    """Plan one step.  `table` dict: lens, mods, ids (arrays over S samples),
+    carry_seq (array over the first n_carry samples: their carry sequence),
+    n_carry_seqs, chunk_off (offsets of drawn chunks, first = n_carry)."""
+    lens = np.asarray(table["lens"], dtype=np.int64)
+    mods = np.asarray(table["mods"], dtype=np.int64)
+    ids = np.asarray(table["ids"], dtype=np.int64)
+    carry_seq = np.asarray(table.get("carry_seq", []), dtype=np.int64)
+    n_carry_seqs = int(table.get("n_carry_seqs", 0))
+    chunk_off = list(table["chunk_off"])
+    S = len(lens)
+    nc = len(carry_seq)
+    if dp * sp != world:
+        raise OracleConfigError(f"llm dp {dp} x sp {sp} != world {world}")
+
+    # oversize: first offender in table order among drawn samples (workload.py:245)
+    for i in range(nc, S):
+        if lens[i] > capacity:
+            raise OraclePackingError(
+                f"sample {ids[i]} ({lens[i]} tokens) exceeds capacity {capacity}")
+
+    seq = np.full(S, -1, np.int64)
+    off = np.zeros(S, np.int64)
+    span = np.zeros(S, np.int64)
+    fills = [0] * n_carry_seqs
+    nspan = [0] * n_carry_seqs
+    for i in range(nc):
+        q = int(carry_seq[i])
+        seq[i], off[i], span[i] = q, fills[q], nspan[q]
+        fills[q] += int(lens[i])
+        nspan[q] += 1
+    base = n_carry_seqs
+    for c in range(len(chunk_off) - 1):
+        lo, hi = chunk_off[c], chunk_off[c + 1]
+        idx = sorted(range(lo, hi), key=lambda i: (-lens[i], ids[i], i))
+        bf = []
+        for i in idx:
+            for b, f in enumerate(bf):
+                if f + lens[i] <= capacity:
+                    break
+            else:
+                b = len(bf)
+                bf.append(0)
+                fills.append(0)
+                nspan.append(0)
+            q = base + b
+            seq[i], off[i], span[i] = q, bf[b], nspan[q]
+            bf[b] += int(lens[i])
+            fills[q] = bf[b]
+            nspan[q] += 1
+        base += len(bf)
+    n_seq = base
+
+    if gbs % (dp * mbs) != 0:
+        raise OracleConfigError(
+            f"global batch {gbs} not divisible by dp {dp} x microbatch size {mbs}")
+    if n_seq < gbs:
+        raise ValueError(f"need {gbs} sequences, have {n_seq}")
+
+    P = gbs // dp
+    fills = np.asarray(fills, dtype=np.int64)
+    in_batch = seq < gbs
+    cu = np.zeros(gbs + 1, np.int64)
+    cu[1:] = np.cumsum(fills[:gbs])
+
+    # Ulysses shard geometry per batch sequence
+    shard_len = np.array([ulysses_split(fills[q], sp) for q in range(gbs)],
+                         dtype=np.int64).reshape(gbs, sp)
+    shard_start = np.zeros((gbs, sp), np.int64)
+    shard_start[:, 1:] = np.cumsum(shard_len[:, :-1], axis=1)
+    # local row base of sequence q on its replica's shard-k rank
+    row_base = np.zeros((gbs, sp), np.int64)
+    llm_rows = np.zeros(world, np.int64)
+    for q in range(gbs):
+        r = q // P
+        for k in range(sp):
+            row_base[q, k] = llm_rows[r * sp + k]
+            llm_rows[r * sp + k] += shard_len[q, k]
+
+    def owner(q, pos):
+        k = int(np.searchsorted(shard_start[q], pos, side="right") - 1)
+        return (q // P) * sp + k, k
+
+    group = np.array([GROUP_OF_MOD[int(m)] for m in mods], dtype=np.int64) if S else \
+        np.zeros(0, np.int64)
+    origin = np.full(S, -1, np.int64)
+    origin_pos = np.full(S, -1, np.int64)
+    for i in range(S):
+        if in_batch[i]:
+            q = int(seq[i])
+            pos = min(int(off[i]), max(int(fills[q]) - 1, 0))
+            origin[i] = owner(q, pos)[0]
+    # origin_pos: (seq, span) order within each origin rank
+    cnt = np.zeros(world, np.int64)
+    for i in sorted(np.flatnonzero(in_batch).tolist(), key=lambda i: (seq[i], span[i])):
+        origin_pos[i] = cnt[origin[i]]
+        cnt[origin[i]] += 1
+
+    enc_item = [i for i in range(S) if in_batch[i] and group[i] >= 0]
+    arena_off = np.full(S, -1, np.int64)
+    arena_rows = np.zeros((world, N_GROUPS), np.int64)
+    for i in enc_item:   # table order
+        arena_off[i] = arena_rows[origin[i], group[i]]
+        arena_rows[origin[i], group[i]] += lens[i]
+
+    enc = np.full(S, -1, np.int64)
+    pools = [enc_item] if pooled else [[i for i in enc_item if group[i] == q]
+                                       for q in range(N_GROUPS)]
+    for items in pools:
+        if not items:
+            continue
+        costs = [float(lens[i]) for i in items]
+        if world == 1:
+            ranks = [0] * len(items)
+        elif method == "lpt":
+            ranks = lpt_assign(costs, [int(ids[i]) for i in items], world)
+        elif method == "kk":
+            ranks = kk_assign(costs, world)
+        else:
+            raise ValueError(f"unknown method {method!r}")
+        for i, r in zip(items, ranks):
+            enc[i] = r
+
+    enc_off = np.full(S, -1, np.int64)
+    recv_rows = np.zeros((world, N_GROUPS), np.int64)
+    for i in sorted(enc_item, key=lambda i: (origin[i], i)):
+        enc_off[i] = recv_rows[enc[i], group[i]]
+        recv_rows[enc[i], group[i]] += lens[i]
+
+    # return pieces: (sample, src row in encoder buffer, dst rank, dst row, rows)
+    pieces = []
+    for i in enc_item:
+        q, r0, L = int(seq[i]), int(off[i]), int(lens[i])
+        t = 0
+        while t < L:
+            pos = r0 + t
+            rank, k = owner(q, pos)
+            n = min(L - t, int(shard_start[q, k] + shard_len[q, k]) - pos)
+            pieces.append((i, int(enc_off[i]) + t, rank,
+                           int(row_base[q, k]) + pos - int(shard_start[q, k]), n))
+            t += n
+    return dict(seq=seq, off=off, span=span, n_seq=n_seq, fills=fills, cu=cu,
+                in_batch=in_batch, origin=origin, origin_pos=origin_pos, group=group,
+                arena_off=arena_off, arena_rows=arena_rows, enc=enc, enc_off=enc_off,
+                recv_rows=recv_rows, llm_rows=llm_rows, shard_len=shard_len,
+                row_base=row_base, pieces=pieces, P=P)
+
+
+def restore_order(plan):
+    """Inverse of the reorder: for every encoder-side row
+    block, where the origin rank keeps it.  Returns {(enc, group, enc_off):
+    (origin, arena_off)}; exactness is checked by composition in the tests."""
+    out = {}
+    for i in np.flatnonzero(plan["enc"] >= 0).tolist():
+        out[(int(plan["enc"][i]), int(plan["group"][i]), int(plan["enc_off"][i]))] = \
+            (int(plan["origin"][i]), int(plan["arena_off"][i]))
+    return out
+
+
+def step_table(carry_seqs, drawn, chunk_sizes, modality_of):
+    """Build a step table from generate_batch-shaped data.  carry_seqs: list of
+    span lists; drawn: list of (id, modality, dataset, length); modality_of:
+    id -> modality string for carry samples."""
+    code = {"text": 0, "image": 1, "video": 2, "audio": 3}
+    lens, mods, ids, carry_seq = [], [], [], []
+    for q, spans in enumerate(carry_seqs):
+        for sid, L in spans:
+            lens.append(L)
+            mods.append(code[modality_of[sid]])
+            ids.append(sid)
+            carry_seq.append(q)
+    nc = len(lens)
+    for sid, m, _, L in drawn:
+        lens.append(L)
+        mods.append(code[m])
+        ids.append(sid)
+    chunk_off = [nc]
+    for n in chunk_sizes:
+        chunk_off.append(chunk_off[-1] + n)
+    return dict(lens=np.array(lens, np.int64), mods=np.array(mods, np.int64),
+                ids=np.array(ids, np.int64), carry_seq=np.array(carry_seq, np.int64),
+                n_carry_seqs=len(carry_seqs), chunk_off=chunk_off)

@@ -1,0 +1,316 @@
+// Segment copies: pack, dispatch, return and scatter of the data path (sm_100a).
+//
+// Every data-plane move of the step is a list of row ranges that are
+// contiguous on both sides: a sample's rows are contiguous in the loader
+// arena, in the encoder buffer and in its packed LLM sequence.  So pack +
+// dispatch (SPEC.md:402 data all-to-all) and return + scatter (SPEC.md:408-416
+// restore, "organized as LLM inputs") are one kernel each: a
+// persistent grid walks fixed-size chunks of the segment table (chunk map
+// built by the planner) and streams bytes with 128-bit loads/stores to a local
+// or NVLink-peer destination pointer.  Rows of 1176 B (588 bf16) are only
+// 8-byte aligned, so a chunk whose source and destination differ mod 16 uses
+// 64-bit accesses; every other chunk uses 128-bit accesses.
+//
+// The last CTA to finish fences at system scope and publishes `epoch` into the
+// completion flag of every peer, so the exchange needs no host round trip.
+
+#include "mux_common.cuh"
+
+namespace mux {
+
+constexpr int kCopyThreads = 256;
+constexpr int kCopyUnroll = 8;  // 8 x 16 B in flight per thread
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_stream2(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+
+// Block-cooperative copy of n bytes; src, dst and n are multiples of 8.
+__device__ __forceinline__ void copy_block(char* dst, const char* src, int64_t n) {
+  const int tid = threadIdx.x;
+  if ((((uintptr_t)src ^ (uintptr_t)dst) & 15) == 0) {
+    int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
+    if (head > n) head = n;
+    if (head && tid == 0) *reinterpret_cast<uint2*>(dst) = ld_stream2(reinterpret_cast<const uint2*>(src));
+    const uint4* s = reinterpret_cast<const uint4*>(src + head);
+    uint4* d = reinterpret_cast<uint4*>(dst + head);
+    const int64_t n16 = (n - head) >> 4;
+    int64_t i = tid;
+    for (; i + (kCopyUnroll - 1) * kCopyThreads < n16; i += kCopyUnroll * kCopyThreads) {
+      uint4 v[kCopyUnroll];
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) v[u] = ld_stream(s + i + u * kCopyThreads);
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) d[i + u * kCopyThreads] = v[u];
+    }
+    for (; i < n16; i += kCopyThreads) d[i] = ld_stream(s + i);
+    const int64_t done = head + (n16 << 4);
+    if (done < n && tid == 0)
+      *reinterpret_cast<uint2*>(dst + done) = ld_stream2(reinterpret_cast<const uint2*>(src + done));
+  } else {
+    const uint2* s = reinterpret_cast<const uint2*>(src);
+    uint2* d = reinterpret_cast<uint2*>(dst);
+    const int64_t n8 = n >> 3;
+    int64_t i = tid;
+    for (; i + (kCopyUnroll - 1) * kCopyThreads < n8; i += kCopyUnroll * kCopyThreads) {
+      uint2 v[kCopyUnroll];
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) v[u] = ld_stream2(s + i + u * kCopyThreads);
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) d[i + u * kCopyThreads] = v[u];
+    }
+    for (; i < n8; i += kCopyThreads) d[i] = ld_stream2(s + i);
+  }
+}
+
+struct SegArgs {
+  const int64_t* hdr_chunks;  // total chunks
+  const int32_t* cmap;
+  const int64_t *chunk0, *src_row, *dst_row, *rows;
+  const int32_t *group, *rank;
+  int64_t chunk_bytes;
+  int32_t row_bytes[MUX_N_GROUPS];
+  int32_t per_group_dst;  // dispatch: dst index = rank*G + group; return: rank
+  void* const* src_bases;
+  void* const* dst_bases;
+  // fused completion signal (optional)
+  uint64_t* const* flags_peers;
+  uint32_t* done_counter;
+  uint64_t epoch;
+  int32_t me, world;
+};
+
+__global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a) {
+  const int64_t nchunks = *a.hdr_chunks;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int s = a.cmap[c];
+    const int g = a.group[s];
+    const int64_t rb = a.row_bytes[g];
+    const int64_t lo = (c - a.chunk0[s]) * a.chunk_bytes;
+    const int64_t seg = a.rows[s] * rb;
+    const int64_t n = seg - lo < a.chunk_bytes ? seg - lo : a.chunk_bytes;
+    const char* src = static_cast<const char*>(a.src_bases[g]) + a.src_row[s] * rb + lo;
+    const int di = a.per_group_dst ? a.rank[s] * MUX_N_GROUPS + g : a.rank[s];
+    char* dst = static_cast<char*>(a.dst_bases[di]) + a.dst_row[s] * rb + lo;
+    copy_block(dst, src, n);
+  }
+  if (a.flags_peers) {
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const uint32_t t = atomicAdd(a.done_counter, 1u);
+      last = t == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x < a.world) {
+      __threadfence_system();
+      uint64_t* f = a.flags_peers[threadIdx.x] + a.me;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.epoch) : "memory");
+      if (threadIdx.x == 0) *a.done_counter = 0;  // re-arm for the next launch
+    }
+  }
+}
+
+__global__ void signal_kernel(int me, int world, uint64_t* const* flags_peers, uint64_t epoch) {
+  const int r = threadIdx.x;
+  if (r < world) {
+    __threadfence_system();
+    uint64_t* f = flags_peers[r] + me;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+  }
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void wait_kernel(int world, const uint64_t* flags, uint64_t epoch, int64_t timeout_ns,
+                            int32_t* err) {
+  const int r = threadIdx.x;
+  if (r >= world) return;
+  const uint64_t t0 = global_ns();
+  for (;;) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + r) : "memory");
+    if (v >= epoch) break;
+    if ((int64_t)(global_ns() - t0) > timeout_ns) {
+      atomicExch(err, 1);
+      break;
+    }
+    __nanosleep(128);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// encoder stand-in E(id, t, c): a deterministic hash mapped to a finite bf16
+// in +-[0.5, 2).  oracle/dataplane.py:standin restates it bit for bit.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x85ebca6bu;
+  x ^= x >> 13;
+  x *= 0xc2b2ae35u;
+  x ^= x >> 16;
+  return x;
+}
+__device__ __forceinline__ uint32_t standin_bits(uint32_t row_seed, uint32_t c) {
+  const uint32_t h = mix32(row_seed ^ (c * 0x85ebca77u));
+  return ((h >> 31) << 15) | ((126u + ((h >> 7) & 1u)) << 7) | (h & 0x7fu);
+}
+
+__global__ void __launch_bounds__(256) standin_kernel(Plan p, int S, int me, int group,
+                                                     const int64_t* ids, const int32_t* lens,
+                                                     int width, uint16_t* out) {
+  for (int i = blockIdx.y; i < S; i += gridDim.y) {
+    if (p.enc[i] != me || p.group[i] != group) continue;
+    const int64_t id = ids[i];
+    const uint32_t sseed = mix32((uint32_t)id ^ mix32((uint32_t)((uint64_t)id >> 32) + 0x632be59bu));
+    const int L = lens[i];
+    const int64_t r0 = p.enc_off[i];
+    const int nv = width / 8;
+    for (int t = blockIdx.x; t < L; t += gridDim.x) {
+      const uint32_t rs = mix32(sseed + (uint32_t)t * 0x9e3779b9u);
+      uint4* row = reinterpret_cast<uint4*>(out + (r0 + t) * width);
+      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const uint32_t c = v * 8;
+        uint4 w;
+        w.x = standin_bits(rs, c) | (standin_bits(rs, c + 1) << 16);
+        w.y = standin_bits(rs, c + 2) | (standin_bits(rs, c + 3) << 16);
+        w.z = standin_bits(rs, c + 4) | (standin_bits(rs, c + 5) << 16);
+        w.w = standin_bits(rs, c + 6) | (standin_bits(rs, c + 7) << 16);
+        row[v] = w;
+      }
+    }
+  }
+}
+
+__global__ void return_rows_kernel(Plan p, int group, int64_t* row_dst, int64_t n_rows) {
+  const int64_t npieces = p.hdr[MUX_H_N_RETURN];
+  for (int64_t s = blockIdx.x; s < npieces; s += gridDim.x) {
+    if (p.rgroup[s] != group) continue;
+    const int64_t src = p.rsrc[s], dst = p.rdst[s], n = p.rrows[s];
+    const int64_t tag = (int64_t)p.rrank[s] << 40;
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x)
+      if (src + t < n_rows) row_dst[src + t] = tag | (dst + t);
+  }
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace mux
+
+using namespace mux;
+
+extern "C" int mux_segcopy(const mux_plan_cfg* cfg, const void* plan, int32_t which,
+                           void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
+                           void* stream) {
+  return mux_segcopy_signal(cfg, plan, which, src_bases, dst_bases, grid_ctas, nullptr, nullptr,
+                            0, stream);
+}
+
+extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
+                                  void* const* src_bases, void* const* dst_bases,
+                                  int32_t grid_ctas, uint64_t* const* flags_peers,
+                                  uint32_t* done_counter, uint64_t epoch, void* stream) {
+  mux_plan_layout L;
+  int st = mux_plan_layout_of(cfg, &L);
+  if (st) return st;
+  Plan p = make_plan_const(plan, L);
+  SegArgs a;
+  const bool ret = which != 0;
+  a.hdr_chunks = p.hdr + (ret ? MUX_H_RETURN_CHUNKS : MUX_H_DISPATCH_CHUNKS);
+  a.cmap = ret ? p.rchunk_seg : p.dchunk_seg;
+  a.chunk0 = ret ? p.rchunk0 : p.dchunk0;
+  a.src_row = ret ? p.rsrc : p.dsrc;
+  a.dst_row = ret ? p.rdst : p.ddst;
+  a.rows = ret ? p.rrows : p.drows;
+  a.group = ret ? p.rgroup : p.dgroup;
+  a.rank = ret ? p.rrank : p.drank;
+  a.chunk_bytes = cfg->chunk_bytes > 0 ? cfg->chunk_bytes : kDefaultChunkBytes;
+  for (int g = 0; g < MUX_N_GROUPS; ++g)
+    a.row_bytes[g] = ret ? cfg->row_bytes_ret[g] : cfg->row_bytes_in[g];
+  a.per_group_dst = ret ? 0 : 1;
+  a.src_bases = src_bases;
+  a.dst_bases = dst_bases;
+  a.flags_peers = flags_peers;
+  a.done_counter = done_counter;
+  a.epoch = epoch;
+  a.me = cfg->me;
+  a.world = cfg->world;
+  if (flags_peers && !done_counter) {
+    set_error("signal requested without a completion counter");
+    return MUX_ERR_VALUE;
+  }
+  const int grid = grid_ctas > 0 ? grid_ctas : num_sms() * 8;
+  segcopy_kernel<<<grid, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t epoch,
+                          void* stream) {
+  signal_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(me, world, flags_peers, epoch);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_wait(int32_t world, const uint64_t* my_flags, uint64_t epoch, int32_t timeout_ms,
+                        int32_t* err_dev, void* stream) {
+  wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(world, my_flags, epoch,
+                                                               (int64_t)timeout_ms * 1000000,
+                                                               err_dev);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, const int64_t* ids,
+                                   const int32_t* lens, int32_t group, int32_t width,
+                                   uint16_t* out, void* stream) {
+  if (width % 8) {
+    set_error("stand-in width %d must be a multiple of 8", width);
+    return MUX_ERR_VALUE;
+  }
+  mux_plan_layout L;
+  int st = mux_plan_layout_of(cfg, &L);
+  if (st) return st;
+  Plan p = make_plan_const(plan, L);
+  dim3 grid(64, cfg->S > 0 ? (cfg->S < 1024 ? cfg->S : 1024) : 1);
+  standin_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, cfg->S, cfg->me, group,
+                                                                      ids, lens, width, out);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_t group,
+                               int64_t* row_dst, int64_t n_rows, void* stream) {
+  mux_plan_layout L;
+  int st = mux_plan_layout_of(cfg, &L);
+  if (st) return st;
+  Plan p = make_plan_const(plan, L);
+  return_rows_kernel<<<256, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, group, row_dst, n_rows);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}

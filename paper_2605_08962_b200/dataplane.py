@@ -1,0 +1,208 @@
+"""The per-step encoder<->LLM data path on B200: plan -> pack+dispatch -> return+scatter.
+
+One process per GPU.  Every rank plans the whole step on its own GPU (the
+plan is integer-only and bit-identical on every rank), then *pushes* its rows:
+
+  pack + dispatch   loader arena rows -> the encoder rank's receive window,
+                    written directly over NVLink (SPEC.md:402 data all-to-all;
+                    PAPER.md:1108-1110 grouped reordering)
+  return + scatter  encoder output rows -> their LLM rank's packed input at the
+                    placeholder positions (SPEC.md:408-416 restore_order and
+                    SPEC.md:462-470 plan_reshard, one hop instead of the
+                    paper's send-then-reshard)
+  projector         with a projector, the return is the tcgen05 GEMM whose
+                    epilogue stores each output row at its (rank, row).
+
+Receive windows, LLM buffers and completion flags are torch symmetric-memory
+allocations (CUDA VMM + IPC under the hood); the kernels get raw peer pointers.
+There is no NCCL on the data path: no counts are exchanged, because every rank
+already knows every offset.  At world 1 the same kernels run on local pointers.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .planner import DeviceTable, Plan, StepTable, make_cfg, plan_step, _stream_ptr
+
+N_GROUPS = _lib.N_GROUPS
+
+
+class _Window:
+    """A buffer every rank can address: local tensor + per-rank pointers."""
+
+    def __init__(self, nbytes: int, device, group=None, world: int = 1):
+        nbytes = max(int(nbytes), 256)
+        if world == 1:
+            self.tensor = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self.ptrs = [self.tensor.data_ptr()]
+            self.handle = None
+        else:
+            import torch.distributed._symmetric_memory as symm
+            self.tensor = symm.empty(nbytes, dtype=torch.uint8, device=device)
+            self.handle = symm.rendezvous(self.tensor, group)
+            me = self.handle.rank
+            delta = self.tensor.data_ptr() - self.handle.buffer_ptrs[me]
+            self.ptrs = [p + delta for p in self.handle.buffer_ptrs]
+
+
+def _ptr_table(ptrs, device) -> torch.Tensor:
+    return torch.tensor([int(p) for p in ptrs], dtype=torch.int64, device=device)
+
+
+class MuxPath:
+    """Per-rank data path for one workload shape.
+
+    capacity/gbs/dp/sp/world follow the reference's GlobalBatch
+    (workload.py:166-183) and the LLM layout of plan_reshard.
+    d_in[g] is the loader row width of encoder group g (0 vision, 1 audio),
+    d_enc[g] the encoder hidden, d_llm the LLM hidden.  projector=False
+    returns d_llm-wide encoder rows bit-exactly; projector=True returns
+    Y = X W_g^T (+ b_g) from d_enc-wide rows.
+    """
+
+    def __init__(self, *, capacity: int, gbs: int, dp: int, sp: int = 1, world: int = 1,
+                 rank: int = 0, method: str = "lpt", pooled: bool = False,
+                 d_in=(588, 512), d_enc=(1280, 1280), d_llm: int = 4096,
+                 projector: bool = False, device=None, group=None, max_rows: int | None = None,
+                 wait_timeout_ms: int = 20000):
+        self.capacity, self.gbs, self.dp, self.sp = capacity, gbs, dp, sp
+        self.world, self.rank, self.method, self.pooled = world, rank, method, pooled
+        self.d_in, self.d_enc, self.d_llm = tuple(d_in), tuple(d_enc), d_llm
+        self.projector = projector
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.group = group
+        self.timeout_ms = wait_timeout_ms
+        self.d_ret = tuple(d_enc) if projector else (d_llm, d_llm)
+        rows = max_rows or gbs * capacity                       # all batch tokens
+        llm_rows = (gbs // dp) * capacity // sp + gbs // dp + 1  # one rank's shards
+        self.max_rows, self.max_llm_rows = rows, llm_rows
+        dev = self.device
+        self.recv = [_Window(rows * d_in[g] * 2, dev, group, world) for g in range(N_GROUPS)]
+        self.llm = _Window(llm_rows * d_llm * 2, dev, group, world)
+        self.flags = _Window(8 * world, dev, group, world)
+        self.flags.tensor.zero_()
+        self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
+                        for g in range(N_GROUPS)]
+        self.done = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        # pointer tables for the copy kernels
+        self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
+                                    for g in range(N_GROUPS)], dev)
+        self.llm_dst = _ptr_table(self.llm.ptrs, dev)
+        self.enc_src = _ptr_table([t.data_ptr() for t in self.enc_out], dev)
+        self.flag_ptrs = _ptr_table(self.flags.ptrs, dev)
+        self.arena_src = torch.zeros(N_GROUPS, dtype=torch.int64, device=dev)
+        self._arena_ptrs = None
+        self.epoch = 0
+        self._plan: Plan | None = None
+        if world > 1:
+            torch.cuda.synchronize()
+            self.flags.handle.barrier()
+        if projector:
+            self.weight = [None] * N_GROUPS
+            self.bias = [None] * N_GROUPS
+            self.row_dst = torch.empty(rows, dtype=torch.int64, device=dev)
+
+    # ------------------------------------------------------------------ setup
+    def set_projector(self, group: int, weight: torch.Tensor, bias: torch.Tensor | None = None):
+        """Projector of encoder group g: weight [d_llm, d_enc] bf16 (nn.Linear layout)."""
+        assert self.projector
+        assert weight.shape == (self.d_llm, self.d_enc[group]) and weight.dtype == torch.bfloat16
+        self.weight[group] = weight.contiguous()
+        self.bias[group] = None if bias is None else bias.contiguous()
+
+    def cfg_for(self, table: StepTable):
+        return make_cfg(table, self.capacity, self.gbs, self.dp, self.sp, self.world, 1,
+                        self.method, self.pooled, self.rank,
+                        row_bytes_in=tuple(2 * d for d in self.d_in),
+                        row_bytes_ret=tuple(2 * d for d in self.d_ret))
+
+    def llm_view(self, rows: int | None = None) -> torch.Tensor:
+        n = self.max_llm_rows if rows is None else rows
+        return self.llm.tensor[: n * self.d_llm * 2].view(torch.bfloat16).view(n, self.d_llm)
+
+    def recv_view(self, group: int, rows: int) -> torch.Tensor:
+        d = self.d_in[group]
+        return self.recv[group].tensor[: rows * d * 2].view(torch.bfloat16).view(rows, d)
+
+    def enc_view(self, group: int, rows: int) -> torch.Tensor:
+        d = self.d_ret[group]
+        return self.enc_out[group][: rows * d].view(rows, d)
+
+    # ------------------------------------------------------------------ stages
+    def plan(self, dtab: DeviceTable, stream=None) -> Plan:
+        cfg = self.cfg_for(dtab.table)
+        self._plan = plan_step(dtab, cfg, self._plan, stream)
+        return self._plan
+
+    def _set_arenas(self, arenas):
+        ptrs = tuple(int(a.data_ptr()) if a is not None else 0 for a in arenas)
+        if ptrs != self._arena_ptrs:
+            self.arena_src.copy_(torch.tensor(ptrs, dtype=torch.int64), non_blocking=False)
+            self._arena_ptrs = ptrs
+
+    def _exchange(self, plan: Plan, which: int, src, dst, stream):
+        L = _lib.lib()
+        s = _stream_ptr(stream)
+        if self.world == 1:
+            _lib.check(L.mux_segcopy(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
+                                     dst.data_ptr(), 0, s), "mux_segcopy")
+            return
+        self.epoch += 1
+        _lib.check(L.mux_segcopy_signal(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
+                                        dst.data_ptr(), 0, self.flag_ptrs.data_ptr(),
+                                        self.done[which:].data_ptr(), self.epoch, s),
+                   "mux_segcopy_signal")
+        _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch,
+                              self.timeout_ms, self.wait_err.data_ptr(), s), "mux_wait")
+
+    def dispatch(self, plan: Plan, arenas, stream=None):
+        """Pack + dispatch: loader rows of every group to their encoder rank."""
+        self._set_arenas(arenas)
+        self._exchange(plan, 0, self.arena_src, self.recv_dst, stream)
+
+    def encode_standin(self, plan: Plan, dtab: DeviceTable, stream=None):
+        """Deterministic encoder stand-in E(id, t, c) into the encoder output."""
+        L = _lib.lib()
+        for g in range(N_GROUPS):
+            _lib.check(L.mux_encoder_standin(C.byref(plan.cfg), plan.ptr, dtab.ids, dtab.lens, g,
+                                             self.d_ret[g], self.enc_out[g].data_ptr(),
+                                             _stream_ptr(stream)), "mux_encoder_standin")
+
+    def return_scatter(self, plan: Plan, recv_rows=None, stream=None):
+        """Return + scatter (projector off) or projector GEMM + scatter (on)."""
+        if not self.projector:
+            self._exchange(plan, 1, self.enc_src, self.llm_dst, stream)
+            return
+        L = _lib.lib()
+        s = _stream_ptr(stream)
+        if recv_rows is None:
+            h = plan.header()
+            recv_rows = (int(h[_lib.H_RECV_ROWS0]), int(h[_lib.H_RECV_ROWS1]))
+        for g in range(N_GROUPS):
+            M = recv_rows[g]
+            if M == 0:
+                continue
+            if self.weight[g] is None:
+                raise RuntimeError(f"projector weight of group {g} not set")
+            _lib.check(L.mux_return_rows(C.byref(plan.cfg), plan.ptr, g, self.row_dst.data_ptr(),
+                                         M, s), "mux_return_rows")
+            b = self.bias[g]
+            _lib.check(L.mux_proj_scatter(self.enc_out[g].data_ptr(), self.weight[g].data_ptr(),
+                                          0 if b is None else b.data_ptr(), M, self.d_enc[g],
+                                          self.d_llm, self.row_dst.data_ptr(),
+                                          self.llm_dst.data_ptr(), 0, s), "mux_proj_scatter")
+        if self.world > 1:
+            self.epoch += 1
+            _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(), self.epoch,
+                                    s), "mux_signal")
+            _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch,
+                                  self.timeout_ms, self.wait_err.data_ptr(), s), "mux_wait")
+
+    def check_wait(self):
+        if int(self.wait_err.item()):
+            raise RuntimeError("cross-GPU completion flag wait timed out")

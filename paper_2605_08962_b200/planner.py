@@ -1,0 +1,273 @@
+"""Device planner: one step table in, one plan blob out (libmuxb200 K_ffd + K_finalize).
+
+A *step table* lists the samples of one training step in table order: the
+carried-over samples first (sequence/span order), then every drawn chunk in
+draw order — exactly what ``generate_batch`` packs
+(pkg/src/muxsim/workload.py:281-305).  The plan holds, bit-identically to
+oracle/planner.py: FFD placement (workload.py:240-262), the global batch and
+replica slice (:265-278, :177-180), Ulysses shard geometry,
+origins, encoder assignment (LPT or KK), encoder order,
+and the segment tables that drive the copy kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import PlanCfg, PlanLayout
+from .configs import GROUP_OF_MOD
+from .workload import MODALITY_CODE, PackedSequence, Sample
+
+METHODS = {"lpt": _lib.LPT, "kk": _lib.KK}
+DEFAULT_CHUNK_BYTES = 32768
+
+
+def _stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+@dataclass
+class StepTable:
+    """Host (numpy) step table."""
+
+    lens: np.ndarray       # int32[S]
+    mods: np.ndarray       # int32[S] modality codes (text 0, image 1, video 2, audio 3)
+    ids: np.ndarray        # int64[S]
+    carry_seq: np.ndarray  # int32[n_carry]
+    n_carry_seqs: int
+    chunk_off: np.ndarray  # int32[n_chunks + 1], chunk_off[0] == n_carry
+
+    @property
+    def S(self) -> int:
+        return int(self.lens.shape[0])
+
+    @property
+    def n_carry(self) -> int:
+        return int(self.carry_seq.shape[0])
+
+    @property
+    def n_chunks(self) -> int:
+        return int(self.chunk_off.shape[0]) - 1
+
+    @staticmethod
+    def from_chunks(carry: list[PackedSequence], chunks: list[list[Sample]],
+                    modality_of: dict | None = None) -> "StepTable":
+        """carry: PackedSequences carried in; chunks: drawn Sample lists;
+        modality_of: sample id -> Modality for the carried samples."""
+        lens, mods, ids, cseq = [], [], [], []
+        for q, seq in enumerate(carry):
+            for sid, tok in seq.spans:
+                lens.append(tok)
+                mods.append(MODALITY_CODE[modality_of[sid]])
+                ids.append(sid)
+                cseq.append(q)
+        off = [len(lens)]
+        for ch in chunks:
+            for s in ch:
+                lens.append(s.length)
+                mods.append(MODALITY_CODE[s.modality])
+                ids.append(s.id)
+            off.append(len(lens))
+        return StepTable(np.asarray(lens, np.int32), np.asarray(mods, np.int32),
+                         np.asarray(ids, np.int64), np.asarray(cseq, np.int32), len(carry),
+                         np.asarray(off, np.int32))
+
+    def blob(self) -> np.ndarray:
+        """One int64 array: ids | int32(lens, mods, carry_seq, chunk_off)."""
+        S, nc, nch = self.S, self.n_carry, self.n_chunks
+        n32 = 2 * S + nc + nch + 1
+        out = np.zeros(S + (n32 + 1) // 2, np.int64)
+        out[:S] = self.ids
+        v = out[S:].view(np.int32)
+        v[:S] = self.lens
+        v[S:2 * S] = self.mods
+        v[2 * S:2 * S + nc] = self.carry_seq
+        v[2 * S + nc:2 * S + nc + nch + 1] = self.chunk_off
+        return out
+
+
+class DeviceTable:
+    """A StepTable resident in device memory (one H2D copy)."""
+
+    def __init__(self, table: StepTable, device, host_blob: torch.Tensor | None = None):
+        """Copy `table` to `device`.  host_blob: the table's blob() already in
+        pinned host memory (the copy is then asynchronous on the current stream)."""
+        self.table = table
+        if host_blob is None:
+            self.blob = torch.from_numpy(table.blob()).to(device)
+        else:
+            self.blob = host_blob.to(device, non_blocking=True)
+        S, nc = table.S, table.n_carry
+        base = self.blob.data_ptr()
+        self.ids = base
+        i32 = base + 8 * S
+        self.lens = i32
+        self.mods = i32 + 4 * S
+        self.carry_seq = i32 + 8 * S
+        self.chunk_off = i32 + 4 * (2 * S + nc)
+
+
+def chunk_bound(capacity: int, gbs: int, sp: int, S: int, row_bytes, chunk_bytes: int) -> int:
+    """Upper bound on copy chunks of one table (all batch tokens, widest row)."""
+    tok = max(gbs, 1) * capacity
+    return (tok * max(row_bytes) + chunk_bytes - 1) // chunk_bytes + S * (sp + 1) + 1
+
+
+def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int = 1,
+             world: int = 1, mbs: int = 1, method: str = "lpt", pooled: bool = False,
+             me: int = 0, mode: int = _lib.MODE_STEP, row_bytes_in=(1176, 1024),
+             row_bytes_ret=(8192, 8192), chunk_bytes: int = DEFAULT_CHUNK_BYTES) -> PlanCfg:
+    if method not in METHODS:
+        raise ValueError(f"unknown balance method {method!r}")
+    c = PlanCfg()
+    c.S, c.n_carry, c.n_carry_seqs, c.n_chunks = table.S, table.n_carry, table.n_carry_seqs, \
+        table.n_chunks
+    c.capacity, c.gbs, c.dp, c.sp, c.world, c.mbs = capacity, gbs, dp, sp, world, mbs
+    c.method, c.pooled, c.me, c.mode = METHODS[method], int(pooled), me, mode
+    for g in range(_lib.N_GROUPS):
+        c.row_bytes_in[g] = row_bytes_in[g]
+        c.row_bytes_ret[g] = row_bytes_ret[g]
+    c.chunk_bytes = chunk_bytes
+    c.max_chunks = max(chunk_bound(capacity, gbs, sp, table.S, row_bytes_in, chunk_bytes),
+                       chunk_bound(capacity, gbs, sp, table.S, row_bytes_ret, chunk_bytes))
+    return c
+
+
+def layout_of(cfg: PlanCfg) -> PlanLayout:
+    L = PlanLayout()
+    _lib.check(_lib.lib().mux_plan_layout_of(C.byref(cfg), C.byref(L)), "plan layout")
+    return L
+
+
+class Plan:
+    """A device plan blob plus typed views of its arrays."""
+
+    I32 = ("seq", "off", "span", "origin", "origin_pos", "group", "enc", "llm_rank",
+           "bin_of", "fills", "nspans", "cu", "shard_len", "shard_start", "dseg_group",
+           "dseg_dst_rank", "rseg_group", "rseg_dst_rank", "chunk_nbins")
+    I64 = ("arena_off", "enc_off", "llm_row", "row_base", "arena_rows", "recv_rows", "llm_rows",
+           "dseg_src_row", "dseg_dst_row", "dseg_rows", "rseg_src_row", "rseg_dst_row",
+           "rseg_rows", "dseg_chunk0", "rseg_chunk0")
+
+    def __init__(self, cfg: PlanCfg, device, blob: torch.Tensor | None = None):
+        self.cfg = cfg
+        self.layout = layout_of(cfg)
+        if blob is None or blob.numel() < self.layout.total:
+            blob = torch.empty(self.layout.total, dtype=torch.uint8, device=device)
+        self.blob = blob
+
+    @property
+    def ptr(self) -> int:
+        return self.blob.data_ptr()
+
+    def view(self, name: str, n: int) -> torch.Tensor:
+        off = getattr(self.layout, name)
+        dt = torch.int64 if name in self.I64 or name == "header" else torch.int32
+        sz = 8 if dt == torch.int64 else 4
+        return self.blob[off:off + sz * n].view(dt)
+
+    def header(self) -> np.ndarray:
+        return self.view("header", _lib.H_SLOTS).cpu().numpy()
+
+    def check(self, table: StepTable) -> np.ndarray:
+        """Synchronise, then raise the reference's exception for a failed plan."""
+        h = np.ascontiguousarray(self.header())
+        st = _lib.lib().mux_plan_check(C.byref(self.cfg), h.ctypes.data,
+                                       np.ascontiguousarray(table.ids).ctypes.data,
+                                       np.ascontiguousarray(table.lens).ctypes.data)
+        _lib.check(st, "plan")
+        return h
+
+    def host(self) -> dict:
+        """All per-sample / per-rank arrays on the host (tests and reporting)."""
+        c, h = self.cfg, self.header()
+        S, W, G = c.S, max(c.world, 1), _lib.N_GROUPS
+        gb = max(c.gbs, 1) * max(c.sp, 1)
+        out = {"header": h}
+        for nm in ("seq", "off", "span", "origin", "origin_pos", "group", "enc", "arena_off",
+                   "enc_off", "llm_rank", "llm_row"):
+            out[nm] = self.view(nm, S).cpu().numpy()
+        nseq = int(h[_lib.H_N_SEQ]) if h[_lib.H_N_SEQ] >= 0 else 0
+        out["fills"] = self.view("fills", nseq).cpu().numpy()
+        out["nspans"] = self.view("nspans", nseq).cpu().numpy()
+        if c.mode == _lib.MODE_STEP and h[_lib.H_STATUS] == 0:
+            out["cu"] = self.view("cu", c.gbs + 1).cpu().numpy()
+            out["shard_len"] = self.view("shard_len", gb).cpu().numpy()
+            out["shard_start"] = self.view("shard_start", gb).cpu().numpy()
+            out["row_base"] = self.view("row_base", gb).cpu().numpy()
+            out["arena_rows"] = self.view("arena_rows", W * G).cpu().numpy().reshape(W, G)
+            out["recv_rows"] = self.view("recv_rows", W * G).cpu().numpy().reshape(W, G)
+            out["llm_rows"] = self.view("llm_rows", W).cpu().numpy()
+            nd, nr = int(h[_lib.H_N_DISPATCH]), int(h[_lib.H_N_RETURN])
+            out["dseg"] = np.stack([self.view("dseg_src_row", nd).cpu().numpy(),
+                                    self.view("dseg_dst_row", nd).cpu().numpy(),
+                                    self.view("dseg_rows", nd).cpu().numpy(),
+                                    self.view("dseg_group", nd).cpu().numpy().astype(np.int64),
+                                    self.view("dseg_dst_rank", nd).cpu().numpy().astype(np.int64)],
+                                   axis=1) if nd else np.zeros((0, 5), np.int64)
+            out["rseg"] = np.stack([self.view("rseg_src_row", nr).cpu().numpy(),
+                                    self.view("rseg_dst_row", nr).cpu().numpy(),
+                                    self.view("rseg_rows", nr).cpu().numpy(),
+                                    self.view("rseg_group", nr).cpu().numpy().astype(np.int64),
+                                    self.view("rseg_dst_rank", nr).cpu().numpy().astype(np.int64)],
+                                   axis=1) if nr else np.zeros((0, 5), np.int64)
+        return out
+
+
+def plan_step(dtab: DeviceTable, cfg: PlanCfg, plan: Plan | None = None, stream=None) -> Plan:
+    """Launch the device planner (stream-ordered, no host sync)."""
+    if plan is None or plan.layout.total < layout_of(cfg).total:
+        plan = Plan(cfg, dtab.blob.device)
+    else:
+        plan.cfg = cfg
+        plan.layout = layout_of(cfg)
+    st = _lib.lib().mux_plan_step(C.byref(cfg), dtab.lens, dtab.mods, dtab.ids, dtab.carry_seq,
+                                  dtab.chunk_off, plan.ptr, plan.blob.numel(),
+                                  _stream_ptr(stream))
+    _lib.check(st, "mux_plan_step")
+    return plan
+
+
+def _spans_from(seq, span, ids, lens, base, nbins, capacity):
+    """PackedSequences of bins [base, base+nbins) from per-sample (seq, span)."""
+    out = [PackedSequence(capacity=capacity) for _ in range(nbins)]
+    order = np.lexsort((span, seq))
+    for i in order.tolist():
+        out[int(seq[i]) - base].spans.append((int(ids[i]), int(lens[i])))
+    return out
+
+
+def device_pack(chunks: list[list[Sample]], capacity: int, device=None):
+    """hybrid_pack of each chunk on the GPU, one launch for all chunks.
+
+    Returns one list of PackedSequences per chunk.  Raises PackingError with
+    the reference's message for the first oversize sample in input order
+    (workload.py:245-248).
+    """
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    table = StepTable.from_chunks([], chunks)
+    cfg = make_cfg(table, capacity, mode=_lib.MODE_PACK)
+    plan = plan_step(DeviceTable(table, device), cfg)
+    h = plan.check(table)
+    S = table.S
+    seq = plan.view("seq", S).cpu().numpy()
+    span = plan.view("span", S).cpu().numpy()
+    nb = plan.view("chunk_nbins", table.n_chunks).cpu().numpy()
+    res, base = [], 0
+    for k in range(table.n_chunks):
+        lo, hi = int(table.chunk_off[k]), int(table.chunk_off[k + 1])
+        res.append(_spans_from(seq[lo:hi], span[lo:hi], table.ids[lo:hi], table.lens[lo:hi],
+                               base, int(nb[k]), capacity))
+        base += int(nb[k])
+    assert base == int(h[_lib.H_N_SEQ])
+    return res
+
+
+def group_of_modality(code: int) -> int:
+    return GROUP_OF_MOD[int(code)]

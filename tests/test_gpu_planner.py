@@ -1,0 +1,150 @@
+"""Device planner parity: every plan array bit-exact against the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import dataplane as odp
+from oracle import planner as oplan
+from oracle import workload as owork
+from paper_2605_08962_b200 import configs, planner, workload as W, balance
+from tests.helpers import golden, golden_steps, oracle_plan, random_table
+
+pytestmark = pytest.mark.gpu
+
+
+def to_table(t):
+    return planner.StepTable(np.asarray(t["lens"], np.int32), np.asarray(t["mods"], np.int32),
+                             np.asarray(t["ids"], np.int64), np.asarray(t["carry_seq"], np.int32),
+                             int(t["n_carry_seqs"]), np.asarray(t["chunk_off"], np.int32))
+
+
+def device_plan(t, cap, gbs, dp, sp, world, me, method="lpt", pooled=False):
+    table = to_table(t)
+    cfg = planner.make_cfg(table, cap, gbs, dp, sp, world, 1, method, pooled, me,
+                           row_bytes_in=(1176, 1024), row_bytes_ret=(8192, 8192))
+    plan = planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
+    plan.check(table)
+    return plan.host()
+
+
+def assert_plan_equal(d, o, t, me):
+    S = len(t["lens"])
+    for k in ("seq", "off", "span"):
+        assert np.array_equal(d[k][:S], o[k]), k
+    assert int(d["header"][2]) == o["n_seq"]
+    assert np.array_equal(d["fills"], o["fills"])
+    inb = o["in_batch"]
+    for k in ("origin", "origin_pos", "enc", "arena_off", "enc_off"):
+        assert np.array_equal(d[k][inb], o[k][inb]), k
+    g = np.asarray(d["group"])
+    assert np.array_equal(g, o["group"])
+    assert np.array_equal(d["cu"], o["cu"])
+    assert np.array_equal(d["arena_rows"], o["arena_rows"])
+    assert np.array_equal(d["recv_rows"], o["recv_rows"])
+    assert np.array_equal(d["llm_rows"], o["llm_rows"])
+    assert np.array_equal(d["row_base"].reshape(o["row_base"].shape), o["row_base"])
+    assert np.array_equal(d["dseg"], odp.dispatch_by_rank(o, t["lens"], me))
+    assert np.array_equal(d["rseg"], odp.pieces_by_rank(o, me))
+
+
+@pytest.mark.parametrize("method", ["lpt", "kk"])
+def test_plan_matches_oracle_on_golden_steps(cuda_device, method):
+    n = 0
+    for name, st, t, _ in golden_steps():
+        o = oracle_plan(t, st, method)
+        world, dp = st["world"], st["dp"]
+        for me in range(world):
+            d = device_plan(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, me, method)
+            assert_plan_equal(d, o, t, me)
+            n += 1
+    assert n > 20
+
+
+def test_plan_matches_oracle_random_tables(cuda_device):
+    rs = np.random.RandomState(11)
+    checked = 0
+    for it in range(120):
+        t, cap = random_table(rs)
+        world, dp = [(1, 1), (2, 2), (2, 1), (4, 4), (4, 2), (8, 8), (8, 2), (8, 1)][it % 8]
+        sp = world // dp
+        gbs = dp * int(rs.randint(1, 3))
+        method = "kk" if it % 3 == 0 else "lpt"
+        pooled = it % 5 == 0
+        try:
+            o = oplan.plan_step(t, cap, gbs, dp, sp, world, 1, method, pooled)
+        except ValueError as e:
+            with pytest.raises(ValueError) as ei:
+                device_plan(t, cap, gbs, dp, sp, world, 0, method, pooled)
+            assert str(ei.value) == str(e)
+            continue
+        me = int(rs.randint(0, world))
+        d = device_plan(t, cap, gbs, dp, sp, world, me, method, pooled)
+        assert_plan_equal(d, o, t, me)
+        checked += 1
+    assert checked > 60
+
+
+def test_plan_errors_match_reference_messages(cuda_device):
+    t = dict(lens=np.array([4, 20, 5, 30]), mods=np.array([1, 1, 1, 1]),
+             ids=np.array([3, 7, 1, 9]), carry_seq=np.zeros(0, np.int64), n_carry_seqs=0,
+             chunk_off=[0, 4])
+    with pytest.raises(W.PackingError, match=r"^sample 7 \(20 tokens\) exceeds capacity 16$"):
+        device_plan(t, 16, 2, 1, 1, 1, 0)
+    t["lens"] = np.array([4, 2, 5, 3])
+    with pytest.raises(W.ConfigError, match="global batch 3 not divisible by dp 2"):
+        device_plan(t, 16, 3, 2, 1, 2, 0)
+    with pytest.raises(ValueError, match=r"^need 4 sequences, have 1$"):
+        device_plan(t, 16, 4, 1, 1, 1, 0)
+
+
+def test_hybrid_pack_matches_reference_golden(cuda_device):
+    P = golden("pack_cases.json")
+    chunks = []
+    for c in P["cases"]:
+        samples = [W.Sample(i, W.Modality.IMAGE, "x", L) for i, L in zip(c["ids"], c["lens"])]
+        got = W.hybrid_pack(samples, c["cap"])
+        assert [[list(sp) for sp in q.spans] for q in got] == c["seqs"]
+        if c["cap"] == 1000:
+            chunks.append((samples, c["seqs"]))
+    # several chunks in one launch (one CTA per chunk)
+    res = planner.device_pack([s for s, _ in chunks], 1000)
+    for (s, want), got in zip(chunks, res):
+        assert [[list(sp) for sp in q.spans] for q in got] == want
+    for e in P["errors"]:
+        samples = [W.Sample(i, W.Modality.AUDIO, "x", L) for i, L in zip(e["ids"], e["lens"])]
+        with pytest.raises(W.PackingError) as ei:
+            W.hybrid_pack(samples, e["cap"])
+        assert str(ei.value) == e["message"]
+
+
+def test_generate_batch_matches_reference_golden(cuda_device):
+    G = golden("configs.json")
+    for name in ("cfg2", "cfg4", "target1", "cfg5"):
+        cfg = configs.CONFIGS[name]
+        reg, sched = configs.build(W, name)
+        recs = [s for s in G[name]["steps"] if s["world"] == (8 if name in ("cfg4", "cfg5") else 1)]
+        carry = None
+        for st in recs:
+            drawn = []
+            b, carry = W.generate_batch(reg, sched, st["step"], cfg["seed"], st["gbs"], st["dp"], 1,
+                                        configs.CAPACITY, carry if cfg["carry"] else None, drawn)
+            assert [[list(sp) for sp in q.spans] for q in b.sequences] == st["batch"]
+            assert [[list(sp) for sp in q.spans] for q in carry] == st["carry_out"]
+            assert [[s.id, s.modality.value, s.dataset, s.length] for s in drawn] == st["drawn"]
+
+
+@pytest.mark.parametrize("method", ["lpt", "kk"])
+def test_partition_matches_oracle(cuda_device, method):
+    rs = np.random.RandomState(5)
+    for _ in range(40):
+        g = int(rs.choice([1, 2, 3, 4, 8]))
+        w = rs.lognormal(7, 1.0, size=int(rs.randint(1, 300))).round().tolist()
+        ids = rs.permutation(len(w)).tolist()
+        if method == "kk":
+            want = oplan.kk_assign([float(x) for x in w], g) if g > 1 else [0] * len(w)
+            got = balance.kk_partition(w, g)
+        else:
+            want = oplan.lpt_assign([float(x) for x in w], ids, g)
+            got = balance.lpt_partition(w, g, ids=ids)
+        assert list(got) == list(want)
+    assert list(balance.kk_partition([8, 7, 6, 5, 4], 2)) == [1, 0, 1, 0, 0]
