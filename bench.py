@@ -219,7 +219,7 @@ def run_ours(args):
         path.dispatch(p, arenas[i], stream)
         if timed_dom is not None:
             timed_dom[0].record(stream)
-        path.return_scatter(p, plans_info[i]["recv"] if projector else None, stream)
+        path.return_scatter(p, stream)
         if timed_dom is not None:
             timed_dom[1].record(stream)
 
@@ -336,7 +336,7 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
             a.copy_(b, non_blocking=True)
         p = path.plan(dt, stream)
         path.dispatch(p, dev_ar[i], stream)
-        path.return_scatter(p, plans_info[i]["recv"] if projector else None, stream)
+        path.return_scatter(p, stream)
         out_hdr.copy_(p.view("header", _lib.H_SLOTS), non_blocking=True)
         return host_tabs[i].numel() * 8 + sum(b.numel() * 2 for b in host_ar[i]), 8 * _lib.H_SLOTS
 

@@ -193,6 +193,13 @@ int mux_proj_scatter(const uint16_t* X, const uint16_t* W, const uint16_t* bias,
                      int32_t K, int32_t N, const int64_t* row_dst, void* const* out_bases,
                      int32_t num_sms, void* stream);
 
+/* Same, with the row count read from device memory at launch (*M_dev,
+ * clamped to M_max) so the step needs no host sync; M_max bounds X. */
+int mux_proj_scatter_dev(const uint16_t* X, const uint16_t* W, const uint16_t* bias,
+                         int64_t M_max, const int64_t* M_dev, int32_t K, int32_t N,
+                         const int64_t* row_dst, void* const* out_bases, int32_t num_sms,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,8 @@ _SIGS = [
     ("mux_return_rows", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, C.c_int64, _P]),
     ("mux_proj_scatter", C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P,
                                    C.c_int32, _P]),
+    ("mux_proj_scatter_dev", C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P,
+                                       C.c_int32, _P]),
 ]
 EXPORTS = tuple(n for n, _, _ in _SIGS)
 

@@ -630,6 +630,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(mux_plan_cfg cfg,
         if (p.shard_start[q * sp + kk] <= pos) k = kk;
       p.origin[i] = (q / P) * sp + k;
       p.scratch_a[i] = k;
+      if (p.group[i] < 0) {  // text: no encoder rows to move
+        p.arena_off[i] = -1;
+        p.enc_off[i] = -1;
+      }
       atomicAdd(&s_cnt[q * sp + k], 1);
       atomicMin(&s_first[q * sp + k], p.span[i]);
     } else {

@@ -1,7 +1,274 @@
-// placeholder, replaced below
+// Projector GEMM fused with the placeholder scatter (sm_100a, tcgen05 + TMEM + TMA).
+//
+//   out[rank(m)][row(m), :] = bf16( X[m, :] . W^T + bias )   for m < M
+//
+// X: encoder output rows in encoder order [M, K]; W: nn.Linear weight [N, K];
+// row_dst[m] = (rank << 40) | row names the packed-LLM position of encoder
+// row m, on this GPU or on an NVLink peer.  There is no reference kernel: the
+// adapter sits between the encoder and the LLM and this
+// fuses it with the return scatter.
+//
+// Persistent, one CTA per SM, warp-specialised:
+//   warp 0      TMA producer: A tile 128x64 and B tile 256x64 per stage
+//               (128-byte swizzle), 4-stage mbarrier ring
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer (M128 N256 K16)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> +bias -> bf16 -> row store
+// Two 256-column fp32 accumulators in TMEM (all 512 columns) let the
+// epilogue of tile i overlap the MMAs of tile i+1.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstring>
+
 #include "mux_common.cuh"
-extern "C" int mux_proj_scatter(const uint16_t*, const uint16_t*, const uint16_t*, int64_t, int32_t,
-                                int32_t, const int64_t*, void* const*, int32_t, void*) {
-  mux::set_error("projector not built");
-  return MUX_ERR_RUNTIME;
+#include "umma.cuh"
+
+namespace mux {
+namespace proj {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int kThreads = 192;
+constexpr int kSmem = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int64_t kRowMask = (1ll << 40) - 1;
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    proj_scatter_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const uint16_t* __restrict__ bias,
+                        int64_t M_max, const int64_t* __restrict__ M_dev, int K, int N,
+                        const int64_t* __restrict__ row_dst, void* const* __restrict__ out_bases) {
+  using namespace umma;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t M = M_max;
+  if (M_dev) {
+    const int64_t m = *M_dev;
+    M = m < M_max ? m : M_max;
+  }
+  const int num_n = N / BN;
+  const int64_t num_tiles = ((M + BM - 1) / BM) * num_n;
+  const int kblocks = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = (int)(tile / num_n), n_blk = (int)(tile % num_n);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full[stage], kb * BK, m_blk * BM, pol_a);
+          tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN, pol_b);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint8_t* sa = smem + stage * STAGE_BYTES;
+          const uint64_t ad = sdesc_sw128(sa), bd = sdesc_sw128(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)  // +32 B per K16 step inside the swizzle atom
+            mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r_in_tile = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = (int)(tile / num_n), n_blk = (int)(tile % num_n);
+      const int64_t m = (int64_t)m_blk * BM + r_in_tile;
+      uint4* dst = nullptr;
+      if (m < M) {
+        const int64_t rd = row_dst[m];
+        char* base = static_cast<char*>(out_bases[rd >> 40]);
+        dst = reinterpret_cast<uint4*>(base + ((rd & kRowMask) * N + (int64_t)n_blk * BN) * 2);
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + j * 32, v);
+        tmem_wait_ld();
+        if (dst) {
+          const int n0 = n_blk * BN + j * 32;
+          uint32_t o[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            float x0 = __uint_as_float(v[2 * c]), x1 = __uint_as_float(v[2 * c + 1]);
+            if (bias) {
+              const uint32_t bb = *reinterpret_cast<const uint32_t*>(bias + n0 + 2 * c);
+              x0 += __uint_as_float(bb << 16);
+              x1 += __uint_as_float(bb & 0xffff0000u);
+            }
+            o[c] = pack_bf16(x0, x1);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            dst[j * 4 + q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        }
+      }
+      fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) tmem_free<512>(tmem_base);
+}
+
+// --- host: tensor maps through the driver entry point (no -lcuda link) --------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return MUX_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return MUX_ERR_CUDA;
+  }
+  return MUX_OK;
+}
+
+}  // namespace proj
+}  // namespace mux
+
+using namespace mux;
+
+extern "C" int mux_proj_scatter(const uint16_t* X, const uint16_t* W, const uint16_t* bias,
+                                int64_t M, int32_t K, int32_t N, const int64_t* row_dst,
+                                void* const* out_bases, int32_t num_sms, void* stream) {
+  return mux_proj_scatter_dev(X, W, bias, M, nullptr, K, N, row_dst, out_bases, num_sms, stream);
+}
+
+extern "C" int mux_proj_scatter_dev(const uint16_t* X, const uint16_t* W, const uint16_t* bias,
+                                    int64_t M_max, const int64_t* M_dev, int32_t K, int32_t N,
+                                    const int64_t* row_dst, void* const* out_bases,
+                                    int32_t num_sms, void* stream) {
+  using namespace proj;
+  if (K % BK || N % BN || K <= 0 || N <= 0 || M_max < 0) {
+    set_error("projector shape M=%lld K=%d N=%d: need K %% %d == 0 and N %% %d == 0",
+              (long long)M_max, K, N, BK, BN);
+    return MUX_ERR_VALUE;
+  }
+  if (M_max == 0) return MUX_OK;
+  CUtensorMap ta, tb;
+  int st = make_map(&ta, X, M_max, K, BM);
+  if (st) return st;
+  st = make_map(&tb, W, N, K, BN);
+  if (st) return st;
+  static bool attr = false;
+  if (!attr) {
+    MUX_CUDA(cudaFuncSetAttribute(proj_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmem));
+    attr = true;
+  }
+  int sms = num_sms;
+  if (sms <= 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t tiles = ((M_max + BM - 1) / BM) * (N / BN);
+  const int grid = (int)(tiles < sms ? tiles : sms);
+  proj_scatter_kernel<<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(
+      ta, tb, bias, M_max, M_dev, K, N, row_dst, out_bases);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
 }

@@ -95,8 +95,7 @@ class MuxPath:
         self.llm_dst = _ptr_table(self.llm.ptrs, dev)
         self.enc_src = _ptr_table([t.data_ptr() for t in self.enc_out], dev)
         self.flag_ptrs = _ptr_table(self.flags.ptrs, dev)
-        self.arena_src = torch.zeros(N_GROUPS, dtype=torch.int64, device=dev)
-        self._arena_ptrs = None
+        self._arena_tables: dict = {}
         self.epoch = 0
         self._plan: Plan | None = None
         if world > 1:
@@ -139,11 +138,15 @@ class MuxPath:
         self._plan = plan_step(dtab, cfg, self._plan, stream)
         return self._plan
 
-    def _set_arenas(self, arenas):
-        ptrs = tuple(int(a.data_ptr()) if a is not None else 0 for a in arenas)
-        if ptrs != self._arena_ptrs:
-            self.arena_src.copy_(torch.tensor(ptrs, dtype=torch.int64), non_blocking=False)
-            self._arena_ptrs = ptrs
+    def _arena_table(self, arenas) -> torch.Tensor:
+        """Device table of loader-arena pointers, cached per arena set (no sync
+        once warm)."""
+        key = tuple(int(a.data_ptr()) if a is not None else 0 for a in arenas)
+        t = self._arena_tables.get(key)
+        if t is None:
+            t = _ptr_table(key, self.device)
+            self._arena_tables[key] = t
+        return t
 
     def _exchange(self, plan: Plan, which: int, src, dst, stream):
         L = _lib.lib()
@@ -162,8 +165,7 @@ class MuxPath:
 
     def dispatch(self, plan: Plan, arenas, stream=None):
         """Pack + dispatch: loader rows of every group to their encoder rank."""
-        self._set_arenas(arenas)
-        self._exchange(plan, 0, self.arena_src, self.recv_dst, stream)
+        self._exchange(plan, 0, self._arena_table(arenas), self.recv_dst, stream)
 
     def encode_standin(self, plan: Plan, dtab: DeviceTable, stream=None):
         """Deterministic encoder stand-in E(id, t, c) into the encoder output."""
@@ -173,29 +175,29 @@ class MuxPath:
                                              self.d_ret[g], self.enc_out[g].data_ptr(),
                                              _stream_ptr(stream)), "mux_encoder_standin")
 
-    def return_scatter(self, plan: Plan, recv_rows=None, stream=None):
-        """Return + scatter (projector off) or projector GEMM + scatter (on)."""
+    def return_scatter(self, plan: Plan, stream=None):
+        """Return + scatter (projector off) or projector GEMM + scatter (on).
+
+        No host synchronisation: row counts are read from the plan header on
+        the device (mux_proj_scatter_dev)."""
         if not self.projector:
             self._exchange(plan, 1, self.enc_src, self.llm_dst, stream)
             return
         L = _lib.lib()
         s = _stream_ptr(stream)
-        if recv_rows is None:
-            h = plan.header()
-            recv_rows = (int(h[_lib.H_RECV_ROWS0]), int(h[_lib.H_RECV_ROWS1]))
+        hdr = plan.ptr + plan.layout.header
         for g in range(N_GROUPS):
-            M = recv_rows[g]
-            if M == 0:
-                continue
             if self.weight[g] is None:
-                raise RuntimeError(f"projector weight of group {g} not set")
+                continue
+            m_dev = hdr + 8 * (_lib.H_RECV_ROWS0 + g)
             _lib.check(L.mux_return_rows(C.byref(plan.cfg), plan.ptr, g, self.row_dst.data_ptr(),
-                                         M, s), "mux_return_rows")
+                                         self.max_rows, s), "mux_return_rows")
             b = self.bias[g]
-            _lib.check(L.mux_proj_scatter(self.enc_out[g].data_ptr(), self.weight[g].data_ptr(),
-                                          0 if b is None else b.data_ptr(), M, self.d_enc[g],
-                                          self.d_llm, self.row_dst.data_ptr(),
-                                          self.llm_dst.data_ptr(), 0, s), "mux_proj_scatter")
+            _lib.check(L.mux_proj_scatter_dev(self.enc_out[g].data_ptr(), self.weight[g].data_ptr(),
+                                              0 if b is None else b.data_ptr(), self.max_rows,
+                                              m_dev, self.d_enc[g], self.d_llm,
+                                              self.row_dst.data_ptr(), self.llm_dst.data_ptr(), 0,
+                                              s), "mux_proj_scatter_dev")
         if self.world > 1:
             self.epoch += 1
             _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(), self.epoch,

@@ -1,0 +1,127 @@
+"""Projector GEMM (tcgen05) fused with the scatter: numerics against a torch fp32
+reference of the same op, and the full cfg2 step against the oracle.
+
+Tolerance (stated): |gpu - ref_fp32| <= 2^-7 * |ref_fp32| + 1e-3, where ref_fp32
+is X.float() @ W.float().T + b with fp32 accumulation; the GPU rounds the fp32
+accumulator to bf16 once (<= 2^-8 relative) and sums K in a different order."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2605_08962_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+RTOL, ATOL = 2.0 ** -7, 1e-3
+
+
+def run_proj(M, K, N, R, bias=True, seed=0, world_rows=None):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    X = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g).to(torch.bfloat16) if bias else None
+    perm = torch.randperm(R, generator=torch.Generator().manual_seed(seed))[:M]
+    out = torch.zeros(R, N, dtype=torch.bfloat16, device="cuda")
+    row_dst = perm.to(torch.int64).cuda()  # rank 0
+    bases = torch.tensor([out.data_ptr()], dtype=torch.int64, device="cuda")
+    st = _lib.lib().mux_proj_scatter(X.data_ptr(), W.data_ptr(), b.data_ptr() if bias else None,
+                                     M, K, N, row_dst.data_ptr(), bases.data_ptr(), 0,
+                                     torch.cuda.current_stream().cuda_stream)
+    _lib.check(st)
+    torch.cuda.synchronize()
+    ref = X.float() @ W.float().t()
+    if bias:
+        ref = ref + b.float()
+    got = out[perm.cuda()].float()
+    err = (got - ref).abs()
+    tol = RTOL * ref.abs() + ATOL
+    assert bool((err <= tol).all()), f"max excess {float((err - tol).max())}"
+    untouched = torch.ones(R, dtype=torch.bool)
+    untouched[perm] = False
+    assert bool((out[untouched.cuda()] == 0).all()), "scatter wrote outside row_dst"
+    return float(err.max())
+
+
+@pytest.mark.parametrize("M,K,N", [(128, 64, 256), (1000, 1280, 512), (4097, 1280, 4096),
+                                   (300, 512, 768)])
+def test_proj_scatter_numerics(cuda_device, M, K, N):
+    run_proj(M, K, N, R=M + 777, bias=(M % 2 == 0))
+
+
+def test_proj_scatter_device_count(cuda_device):
+    """M read from device memory: rows >= *M_dev are neither computed nor stored."""
+    M_max, K, N = 1024, 256, 256
+    X = torch.randn(M_max, K, device="cuda").to(torch.bfloat16)
+    W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    out = torch.zeros(M_max, N, dtype=torch.bfloat16, device="cuda")
+    row_dst = torch.arange(M_max, dtype=torch.int64, device="cuda")
+    bases = torch.tensor([out.data_ptr()], dtype=torch.int64, device="cuda")
+    m_dev = torch.tensor([517], dtype=torch.int64, device="cuda")
+    st = _lib.lib().mux_proj_scatter_dev(X.data_ptr(), W.data_ptr(), None, M_max, m_dev.data_ptr(),
+                                         K, N, row_dst.data_ptr(), bases.data_ptr(), 0,
+                                         torch.cuda.current_stream().cuda_stream)
+    _lib.check(st)
+    torch.cuda.synchronize()
+    ref = (X[:517].float() @ W.float().t())
+    assert bool(((out[:517].float() - ref).abs() <= RTOL * ref.abs() + ATOL).all())
+    assert bool((out[517:] == 0).all())
+
+
+def test_proj_rejects_bad_shapes(cuda_device):
+    with pytest.raises(ValueError):
+        _lib.check(_lib.lib().mux_proj_scatter(None, None, None, 10, 100, 256, None, None, 0, None))
+
+
+def test_cfg2_step_with_projector_matches_oracle(cuda_device):
+    """Full cfg2 step (ViT-600M -> 7B shapes): plan, pack, stand-in, projector+scatter."""
+    from oracle import dataplane as odp
+    from oracle import planner as oplan
+    from paper_2605_08962_b200 import configs, planner
+    from paper_2605_08962_b200.dataplane import MuxPath
+    from tests.helpers import golden_steps
+    from tests.test_gpu_planner import to_table
+
+    for name, st, t, _ in golden_steps():
+        if name != "cfg2" or st["step"] != 1:
+            continue
+        cap, gbs = configs.CAPACITY, st["gbs"]
+        d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, configs.D_LLM
+        o = oplan.plan_step(t, cap, gbs, 1, 1, 1)
+        path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_enc=d_enc, d_llm=d_llm,
+                       projector=True)
+        g = torch.Generator().manual_seed(3)
+        Ws = [(torch.randn(d_llm, d_enc[k], generator=g) / d_enc[k] ** 0.5).to(torch.bfloat16)
+              for k in range(2)]
+        bs = [torch.randn(d_llm, generator=g).to(torch.bfloat16) for k in range(2)]
+        for k in range(2):
+            path.set_projector(k, Ws[k].cuda(), bs[k].cuda())
+        arenas = [torch.randn(max(int(o["arena_rows"][0, k]), 1), d_in[k], generator=g)
+                  .to(torch.bfloat16) for k in range(2)]
+        table = to_table(t)
+        dtab = planner.DeviceTable(table, "cuda")
+        plan = path.plan(dtab)
+        plan.check(table)
+        path.llm_view().zero_()
+        path.dispatch(plan, [a.cuda() for a in arenas])
+        path.encode_standin(plan, dtab)
+        path.return_scatter(plan)
+        torch.cuda.synchronize()
+        # reference in torch fp32 on the GPU from the (bit-exact) encoder rows
+        n = int(o["llm_rows"][0])
+        got = path.llm_view(n).float()
+        ref = torch.zeros(n, d_llm, device="cuda")
+        for (i, src, dst_rank, dst_row, rows) in o["pieces"]:
+            k = int(o["group"][i])
+            x = torch.from_numpy(odp.standin(int(t["ids"][i]), int(t["lens"][i]), d_enc[k])
+                                 .view(np.int16)).view(torch.bfloat16).cuda()[:rows]
+            ref[dst_row:dst_row + rows] = x.float() @ Ws[k].cuda().float().t() + bs[k].cuda().float()
+        err = (got - ref).abs()
+        assert bool((err <= RTOL * ref.abs() + ATOL).all()), float((err - RTOL * ref.abs()).max())
+        mask = torch.zeros(n, dtype=torch.bool, device="cuda")
+        for (i, src, dst_rank, dst_row, rows) in o["pieces"]:
+            mask[dst_row:dst_row + rows] = True
+        assert bool((got[~mask] == 0).all())
+        return
+    raise AssertionError("cfg2 golden step missing")
