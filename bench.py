@@ -82,47 +82,86 @@ def generate_steps(name, world, n_steps):
 # clocks sampling (nvidia-smi during the timed region)
 # ----------------------------------------------------------------------------
 
-class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index):
-        self.index, self.rows, self.stop = index, [], threading.Event()
-
-    def _run(self):
-        while not self.stop.is_set():
+def _clock_proc(index, q, stop, period):
+    """Child process: sample SM clock / throttle reasons until `stop` is set."""
+    reasons = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+    sm, seen, mx, src = [], set(), None, "nvml"
+    try:
+        import pynvml as n
+        n.nvmlInit()
+        h = n.nvmlDeviceGetHandleByIndex(index)
+        mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+        q.put("ready")
+        while not stop.is_set():
+            sm.append(n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM))
+            r = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+            seen.update(k for k, b in reasons.items() if r & b)
+            time.sleep(period)
+    except Exception as e:  # no NVML: nvidia-smi polling
+        src = f"nvidia-smi ({type(e).__name__})"
+        try:
+            q.put("ready")
+        except Exception:
+            pass
+        qq = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not stop.is_set():
             try:
-                r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                r = subprocess.run(["nvidia-smi", "-i", str(index), f"--query-gpu={qq}",
                                     "--format=csv,noheader,nounits"], capture_output=True,
                                    text=True, timeout=5)
-                if r.returncode == 0 and r.stdout.strip():
-                    self.rows.append([x.strip() for x in r.stdout.strip().split(",")])
+                f = [x.strip() for x in r.stdout.strip().split(",")]
+                sm.append(float(f[0]))
+                mx = float(f[1])
+                seen.update(nm for k, nm in enumerate(names)
+                            if f[2 + k].lower().startswith("active"))
             except Exception:
                 pass
-            self.stop.wait(0.1)
+            time.sleep(0.05)
+    q.put({"sm": sm, "mx": mx, "reasons": sorted(seen), "source": src})
+
+
+class Clocks:
+    """SM clocks and throttle reasons sampled by a child process (no GIL
+    contention with the launch loop) from before warm-up to the end of the
+    timed region."""
+
+    def __init__(self, index, period=0.001):
+        import multiprocessing as mp
+        ctx = mp.get_context("spawn")
+        self.q, self.stop = ctx.Queue(), ctx.Event()
+        self.p = ctx.Process(target=_clock_proc, args=(index, self.q, self.stop, period),
+                             daemon=True)
+        self.res = None
 
     def __enter__(self):
-        self.t = threading.Thread(target=self._run, daemon=True)
-        self.t.start()
+        self.p.start()
+        try:
+            self.q.get(timeout=60)
+        except Exception:
+            pass
         return self
 
     def __exit__(self, *a):
         self.stop.set()
-        self.t.join(timeout=10)
+        try:
+            self.res = self.q.get(timeout=30)
+        except Exception:
+            self.res = None
+        self.p.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+        r = self.res
+        if not r or not r["sm"]:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"],
                     "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4)
-                          if len(r) > 5 + k and r[5 + k].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        return {"sm_mhz": float(np.median(r["sm"])), "sm_min_mhz": float(min(r["sm"])),
+                "sm_max_mhz": float(r["mx"]) if r["mx"] else None, "reasons": r["reasons"],
+                "samples": len(r["sm"]), "source": r["source"],
+                "window": "warm-up + 100 ms soak + timed region"}
 
 
 def peaks():
@@ -223,13 +262,21 @@ def run_ours(args):
         if timed_dom is not None:
             timed_dom[1].record(stream)
 
-    for k in range(args.warmup):
-        one_step(k)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    clk = Clocks(local)
+    with clk:
+        t0.record(stream)
+        for k in range(args.warmup):
+            one_step(k)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        # untimed soak (~100 ms) so the clock record covers a loaded GPU
+        est = max(t0.elapsed_time(t1) / max(args.warmup, 1), 0.01)
+        for k in range(int(min(100.0 / est, 5000))):
+            one_step(k)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0.record(stream)
         for k in range(args.steps):
@@ -244,6 +291,22 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
         dist.barrier()
+
+    # per-stage breakdown (separate untimed pass, CUDA events between stages)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for k in range(args.steps):
+        i = (args.warmup + k) % n_distinct
+        ev[k][0].record(stream)
+        p = path.plan(dtabs[i], stream)
+        ev[k][1].record(stream)
+        path.dispatch(p, arenas[i], stream)
+        ev[k][2].record(stream)
+        path.return_scatter(p, stream)
+        ev[k][3].record(stream)
+    torch.cuda.synchronize()
+    stages = {nm: float(np.mean([e[j].elapsed_time(e[j + 1]) for e in ev]))
+              for j, nm in enumerate(("plan_ms", "pack_dispatch_ms",
+                                      "projector_scatter_ms" if projector else "return_scatter_ms"))}
 
     steps_idx = [(args.warmup + k) % n_distinct for k in range(args.steps)]
     M_total = sum(plans_info[i]["M"] for i in steps_idx)
@@ -299,6 +362,7 @@ def run_ours(args):
                    "llm_tokens_per_step": T_total / args.steps,
                    "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"},
         "roofline": roof,
+        "stages": stages,
         "gpu_launches": launches * args.steps,
         "e2e": e2e,
     }

@@ -151,24 +151,27 @@ int mux_assign(int32_t method, const double* weights, const int64_t* ids, int32_
 int mux_segcopy(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                 void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
                 void* stream);
-/* Same copy, then the last CTA fences at system scope and stores `epoch`
- * into flags_peers[r][me] for every rank r (fused completion signal).
+/* Same copy, then the last CTA advances the device epoch counter
+ * (e = ++*epoch_ctr), fences at system scope and stores e into
+ * flags_peers[r][me] for every rank r (fused completion signal).
  * done_counter: one zero-initialised uint32 in device memory, re-armed by
- * the kernel itself. */
+ * the kernel itself.  Epochs live in device memory, so a captured CUDA graph
+ * of the step replays correctly. */
 int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                        void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
-                       uint64_t* const* flags_peers, uint32_t* done_counter, uint64_t epoch,
-                       void* stream);
+                       uint64_t* const* flags_peers, uint32_t* done_counter,
+                       uint64_t* epoch_ctr, void* stream);
 
 /* Cross-GPU completion flags.  flags_peers: device array of `world` device
  * pointers to each rank's uint64 flag array (world entries each).  signal
- * stores `epoch` into flag[me] of every peer after a system-scope fence;
- * wait spins until every flag[src] of `my_flags` >= epoch (bounded:
- * timeout_ms, status written to *err_dev). */
-int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t epoch,
+ * advances the device epoch counter (e = ++*epoch_ctr) and stores e into
+ * flag[me] of every peer after a system-scope fence; wait spins until every
+ * flag[src] of `my_flags` >= *epoch_ctr (bounded: timeout_ms; a timeout sets
+ * *err_dev = 1 and returns). */
+int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t* epoch_ctr,
                void* stream);
-int mux_wait(int32_t world, const uint64_t* my_flags, uint64_t epoch, int32_t timeout_ms,
-             int32_t* err_dev, void* stream);
+int mux_wait(int32_t world, const uint64_t* my_flags, const uint64_t* epoch_ctr,
+             int32_t timeout_ms, int32_t* err_dev, void* stream);
 
 /* Deterministic encoder stand-in: for every sample of rank `me` in group
  * `group`, rows [enc_off, enc_off+len) of out (row width `width` bf16)

@@ -32,7 +32,8 @@ constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int kThreads = 192;
-constexpr int kSmem = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int kStagingBytes = 4 * 32 * 256;  // epilogue: 4 warps x 32 rows x 256 B
+constexpr int kSmem = STAGES * STAGE_BYTES + 256 + kStagingBytes + 1024;
 constexpr int64_t kRowMask = (1ll << 40) - 1;
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -86,7 +87,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+      // A (128-row block) is re-read by the 16 N-tiles that run concurrently on other
+      // CTAs and W (10.5 MB) by every tile: keep both in L2.
+      const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -135,34 +138,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
+    // Epilogue: TMEM -> registers (+bias, bf16) -> warp-private smem staging
+    // (XOR-swizzled, conflict-free) -> coalesced 256-byte row segments to the
+    // destination row, local or NVLink peer (full 128-B lines on the wire).
     const int quarter = warp & 3;
-    const int r_in_tile = quarter * 32 + lane;
+    uint4* stage = reinterpret_cast<uint4*>(smem + STAGES * STAGE_BYTES + 256) +
+                   (warp - 2) * (32 * 16);  // [32 rows][16 x uint4] = 8 KB per warp
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m_blk = (int)(tile / num_n), n_blk = (int)(tile % num_n);
-      const int64_t m = (int64_t)m_blk * BM + r_in_tile;
-      uint4* dst = nullptr;
+      const int64_t m = (int64_t)m_blk * BM + quarter * 32 + lane;
+      char* my_dst = nullptr;
       if (m < M) {
         const int64_t rd = row_dst[m];
-        char* base = static_cast<char*>(out_bases[rd >> 40]);
-        dst = reinterpret_cast<uint4*>(base + ((rd & kRowMask) * N + (int64_t)n_blk * BN) * 2);
+        my_dst = static_cast<char*>(out_bases[rd >> 40]) +
+                 ((rd & kRowMask) * N + (int64_t)n_blk * BN) * 2;
       }
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + j * 32, v);
-        tmem_wait_ld();
-        if (dst) {
-          const int n0 = n_blk * BN + j * 32;
+      for (int half = 0; half < 2; ++half) {
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+          uint32_t v[32];
+          const int col = half * 128 + j * 32;
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + col, v);
+          tmem_wait_ld();
+          const int n0 = n_blk * BN + col;
           uint32_t o[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             float x0 = __uint_as_float(v[2 * c]), x1 = __uint_as_float(v[2 * c + 1]);
             if (bias) {
-              const uint32_t bb = *reinterpret_cast<const uint32_t*>(bias + n0 + 2 * c);
+              const uint32_t bb = __ldg(reinterpret_cast<const uint32_t*>(bias + n0 + 2 * c));
               x0 += __uint_as_float(bb << 16);
               x1 += __uint_as_float(bb & 0xffff0000u);
             }
@@ -170,8 +179,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            dst[j * 4 + q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            stage[lane * 16 + ((j * 4 + q) ^ (lane & 7))] =
+                make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         }
+        __syncwarp();
+        // two rows per iteration: lanes 0-15 row r, lanes 16-31 row r+1
+        const int sub = lane >> 4, c16 = lane & 15;
+#pragma unroll 4
+        for (int r = 0; r < 32; r += 2) {
+          const int row = r + sub;
+          char* d = reinterpret_cast<char*>(__shfl_sync(MUX_FULL, (unsigned long long)my_dst, row));
+          const uint4 val = stage[row * 16 + (c16 ^ (row & 7))];
+          if (d) *reinterpret_cast<uint4*>(d + half * 256 + c16 * 16) = val;
+        }
+        __syncwarp();
       }
       fence_before();
       mbar_arrive(&tempty[acc]);

@@ -87,7 +87,7 @@ struct SegArgs {
   // fused completion signal (optional)
   uint64_t* const* flags_peers;
   uint32_t* done_counter;
-  uint64_t epoch;
+  uint64_t* epoch_ctr;  // device counter: epoch = ++*epoch_ctr (graph-replay safe)
   int32_t me, world;
 };
 
@@ -106,29 +106,40 @@ __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a) {
     copy_block(dst, src, n);
   }
   if (a.flags_peers) {
+    __threadfence_system();  // every thread's peer stores before the CTA's arrival
     __syncthreads();
     __shared__ bool last;
     if (threadIdx.x == 0) {
-      __threadfence_system();
       const uint32_t t = atomicAdd(a.done_counter, 1u);
       last = t == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x < a.world) {
+    if (last && threadIdx.x < 32) {
+      const uint64_t e = *a.epoch_ctr + 1;
+      __syncwarp();
+      if (threadIdx.x == 0) {
+        *a.epoch_ctr = e;
+        *a.done_counter = 0;  // re-arm for the next launch
+      }
       __threadfence_system();
-      uint64_t* f = a.flags_peers[threadIdx.x] + a.me;
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.epoch) : "memory");
-      if (threadIdx.x == 0) *a.done_counter = 0;  // re-arm for the next launch
+      if (threadIdx.x < a.world) {
+        uint64_t* f = a.flags_peers[threadIdx.x] + a.me;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+      }
     }
   }
 }
 
-__global__ void signal_kernel(int me, int world, uint64_t* const* flags_peers, uint64_t epoch) {
+__global__ void signal_kernel(int me, int world, uint64_t* const* flags_peers,
+                              uint64_t* epoch_ctr) {
   const int r = threadIdx.x;
+  const uint64_t e = *epoch_ctr + 1;
+  __syncwarp();
+  if (r == 0) *epoch_ctr = e;
+  __threadfence_system();
   if (r < world) {
-    __threadfence_system();
     uint64_t* f = flags_peers[r] + me;
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
   }
 }
 
@@ -138,10 +149,11 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
-__global__ void wait_kernel(int world, const uint64_t* flags, uint64_t epoch, int64_t timeout_ns,
-                            int32_t* err) {
+__global__ void wait_kernel(int world, const uint64_t* flags, const uint64_t* epoch_ctr,
+                            int64_t timeout_ns, int32_t* err) {
   const int r = threadIdx.x;
   if (r >= world) return;
+  const uint64_t epoch = *epoch_ctr;
   const uint64_t t0 = global_ns();
   for (;;) {
     uint64_t v;
@@ -228,13 +240,13 @@ extern "C" int mux_segcopy(const mux_plan_cfg* cfg, const void* plan, int32_t wh
                            void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
                            void* stream) {
   return mux_segcopy_signal(cfg, plan, which, src_bases, dst_bases, grid_ctas, nullptr, nullptr,
-                            0, stream);
+                            nullptr, stream);
 }
 
 extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                                   void* const* src_bases, void* const* dst_bases,
                                   int32_t grid_ctas, uint64_t* const* flags_peers,
-                                  uint32_t* done_counter, uint64_t epoch, void* stream) {
+                                  uint32_t* done_counter, uint64_t* epoch_ctr, void* stream) {
   mux_plan_layout L;
   int st = mux_plan_layout_of(cfg, &L);
   if (st) return st;
@@ -257,11 +269,11 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
   a.dst_bases = dst_bases;
   a.flags_peers = flags_peers;
   a.done_counter = done_counter;
-  a.epoch = epoch;
+  a.epoch_ctr = epoch_ctr;
   a.me = cfg->me;
   a.world = cfg->world;
-  if (flags_peers && !done_counter) {
-    set_error("signal requested without a completion counter");
+  if (flags_peers && (!done_counter || !epoch_ctr)) {
+    set_error("signal requested without completion/epoch counters");
     return MUX_ERR_VALUE;
   }
   const int grid = grid_ctas > 0 ? grid_ctas : num_sms() * 8;
@@ -270,16 +282,17 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
   return MUX_OK;
 }
 
-extern "C" int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t epoch,
-                          void* stream) {
-  signal_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(me, world, flags_peers, epoch);
+extern "C" int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers,
+                          uint64_t* epoch_ctr, void* stream) {
+  signal_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(me, world, flags_peers,
+                                                                 epoch_ctr);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }
 
-extern "C" int mux_wait(int32_t world, const uint64_t* my_flags, uint64_t epoch, int32_t timeout_ms,
-                        int32_t* err_dev, void* stream) {
-  wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(world, my_flags, epoch,
+extern "C" int mux_wait(int32_t world, const uint64_t* my_flags, const uint64_t* epoch_ctr,
+                        int32_t timeout_ms, int32_t* err_dev, void* stream) {
+  wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(world, my_flags, epoch_ctr,
                                                                (int64_t)timeout_ms * 1000000,
                                                                err_dev);
   MUX_CUDA(cudaGetLastError());

@@ -88,6 +88,7 @@ class MuxPath:
         self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
                         for g in range(N_GROUPS)]
         self.done = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
         # pointer tables for the copy kernels
         self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
@@ -96,7 +97,6 @@ class MuxPath:
         self.enc_src = _ptr_table([t.data_ptr() for t in self.enc_out], dev)
         self.flag_ptrs = _ptr_table(self.flags.ptrs, dev)
         self._arena_tables: dict = {}
-        self.epoch = 0
         self._plan: Plan | None = None
         if world > 1:
             torch.cuda.synchronize()
@@ -155,12 +155,11 @@ class MuxPath:
             _lib.check(L.mux_segcopy(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
                                      dst.data_ptr(), 0, s), "mux_segcopy")
             return
-        self.epoch += 1
         _lib.check(L.mux_segcopy_signal(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
                                         dst.data_ptr(), 0, self.flag_ptrs.data_ptr(),
-                                        self.done[which:].data_ptr(), self.epoch, s),
-                   "mux_segcopy_signal")
-        _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch,
+                                        self.done[which:].data_ptr(), self.epoch_ctr.data_ptr(),
+                                        s), "mux_segcopy_signal")
+        _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch_ctr.data_ptr(),
                               self.timeout_ms, self.wait_err.data_ptr(), s), "mux_wait")
 
     def dispatch(self, plan: Plan, arenas, stream=None):
@@ -199,11 +198,11 @@ class MuxPath:
                                               self.row_dst.data_ptr(), self.llm_dst.data_ptr(), 0,
                                               s), "mux_proj_scatter_dev")
         if self.world > 1:
-            self.epoch += 1
-            _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(), self.epoch,
-                                    s), "mux_signal")
-            _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch,
-                                  self.timeout_ms, self.wait_err.data_ptr(), s), "mux_wait")
+            _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(),
+                                    self.epoch_ctr.data_ptr(), s), "mux_signal")
+            _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(),
+                                  self.epoch_ctr.data_ptr(), self.timeout_ms,
+                                  self.wait_err.data_ptr(), s), "mux_wait")
 
     def check_wait(self):
         if int(self.wait_err.item()):

@@ -1,0 +1,106 @@
+"""torchrun worker: the multi-GPU push exchange, bit-exact per rank against the oracle.
+
+    torchrun --nproc-per-node N tests/mgpu_worker.py [config] [projector]
+
+Every rank plans the whole step on its GPU, pushes its loader rows into the
+encoder ranks' receive windows over NVLink, runs the stand-in encoder, and
+pushes the returned rows into their LLM ranks' packed buffers.  Each rank then
+checks its own receive windows and LLM buffer against the fake-world oracle
+(which every rank can compute: all inputs are seeded).
+"""
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import dataplane as odp  # noqa: E402
+from oracle import planner as oplan  # noqa: E402
+from oracle import workload as owork  # noqa: E402
+from paper_2605_08962_b200 import configs, planner  # noqa: E402
+from paper_2605_08962_b200.dataplane import MuxPath  # noqa: E402
+
+
+def payload(rows, width, seed):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randn(max(rows, 1), width, generator=g).to(torch.bfloat16)
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
+    narrow = "narrow" in sys.argv
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    cfg = configs.CONFIGS[name]
+    sp = cfg["sp"] if world % cfg["sp"] == 0 and world >= cfg["sp"] else 1
+    dp = world // sp
+    gbs = cfg["gbs_per_replica"] * dp
+    d_in = (20, 8) if narrow else configs.D_IN
+    d_llm = 64 if narrow else 512
+    descs = owork.descs_from_config(configs.DATASETS, cfg["datasets"])
+    carry, seen = None, {}
+    path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
+                   d_in=d_in, d_llm=d_llm, device=dev, group=dist.group.WORLD)
+    fails = 0
+    for step in range(3):
+        _, rest, drawn, chunks = owork.generate(descs, cfg["phases"], False, step, cfg["seed"],
+                                                gbs, dp, 1, configs.CAPACITY,
+                                                carry if cfg["carry"] else None)
+        for s in drawn:
+            seen[s[0]] = s[1]
+        t = oplan.step_table(list(carry or []) if cfg["carry"] else [], drawn, chunks, seen)
+        carry = rest
+        for method in ("lpt", "kk"):
+            path.method = method
+            o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
+            arenas = [[payload(int(o["arena_rows"][r, g]), d_in[g], 1000 * step + 10 * r + g)
+                       for g in range(2)] for r in range(world)]
+            table = planner.StepTable(t["lens"].astype(np.int32), t["mods"].astype(np.int32),
+                                      t["ids"], t["carry_seq"].astype(np.int32),
+                                      t["n_carry_seqs"], np.asarray(t["chunk_off"], np.int32))
+            dtab = planner.DeviceTable(table, dev)
+            plan = path.plan(dtab)
+            plan.check(table)
+            path.llm_view().zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            path.dispatch(plan, [a.to(dev) for a in arenas[rank]])
+            path.encode_standin(plan, dtab)
+            path.return_scatter(plan)
+            torch.cuda.synchronize()
+            path.check_wait()
+            ar = [[a.view(torch.int16).numpy().view(np.uint16) for a in arenas[r]]
+                  for r in range(world)]
+            recv, _, llm = odp.run_world(o, t, world, ar, d_in, (d_llm, d_llm), d_llm)
+            for g in range(2):
+                n = int(o["recv_rows"][rank, g])
+                got = path.recv_view(g, n).cpu().view(torch.int16).numpy().view(np.uint16)
+                if not np.array_equal(got, recv[rank][g]):
+                    print(f"rank {rank} step {step} {method}: recv group {g} differs", flush=True)
+                    fails += 1
+            n = int(o["llm_rows"][rank])
+            got = path.llm_view(n).cpu().view(torch.int16).numpy().view(np.uint16)
+            if not np.array_equal(got, llm[rank]):
+                print(f"rank {rank} step {step} {method}: llm buffer differs", flush=True)
+                fails += 1
+            moved = int(o["recv_rows"].sum())
+            if rank == 0:
+                print(f"step {step} {method}: {moved} modality tokens over {world} ranks ok="
+                      f"{fails == 0}", flush=True)
+            dist.barrier()
+    t = torch.tensor([fails], device=dev)
+    dist.all_reduce(t)
+    dist.destroy_process_group()
+    sys.exit(1 if int(t.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()
