@@ -83,18 +83,18 @@ typedef struct {
   int32_t mode;         /* MUX_MODE_PACK | MUX_MODE_STEP                    */
   int32_t row_bytes_in[MUX_N_GROUPS];  /* loader row bytes per group        */
   int32_t row_bytes_ret[MUX_N_GROUPS]; /* returned row bytes per group      */
-  int32_t chunk_bytes;  /* copy work unit (0 = default)                     */
-  int32_t max_chunks;   /* capacity of each chunk map                       */
+  int32_t chunk_bytes;  /* copy work unit (0 = default 32 KiB)              */
 } mux_plan_cfg;
 
 /* Byte offsets of every array inside the plan buffer (one device blob). */
 typedef struct {
   int64_t header;                                   /* int64[MUX_H_SLOTS] */
+  int64_t sync;     /* uint32 ticket; must be zero when the blob is first used */
   int64_t seq, off, span, origin, origin_pos, group, enc; /* int32[S]      */
   int64_t arena_off, enc_off;                       /* int64[S]           */
   int64_t llm_rank, llm_row;                        /* int32/int64[S]     */
   int64_t bin_fill, bin_nspan, bin_of;              /* int32[S] (scratch) */
-  int64_t chunk_nbins;                              /* int32[n_chunks]    */
+  int64_t chunk_nbins, chunk_err;                   /* int32[n_chunks]    */
   int64_t fills, nspans;                            /* int32[max_seq]     */
   int64_t cu;                                       /* int32[gbs+1]       */
   int64_t shard_len, shard_start;                   /* int32[gbs*sp]      */
@@ -105,13 +105,11 @@ typedef struct {
   /* dispatch segments (rank me): rows from arena[group] to recv[group]@enc */
   int64_t dseg_src_row, dseg_dst_row, dseg_rows;    /* int64[S]           */
   int64_t dseg_group, dseg_dst_rank;                /* int32[S]           */
-  int64_t dseg_chunk0;                              /* int64[S+1]         */
-  int64_t dchunk_seg;                               /* int32[max_chunks]  */
+  int64_t dseg_chunk0;  /* int64[S+1]: first copy chunk of each segment   */
   /* return pieces (rank me): rows from enc_out[group] to llm@dst_rank      */
   int64_t rseg_src_row, rseg_dst_row, rseg_rows;    /* int64[S*(sp+1)]    */
   int64_t rseg_group, rseg_dst_rank;                /* int32[S*(sp+1)]    */
   int64_t rseg_chunk0;                              /* int64[S*(sp+1)+1]  */
-  int64_t rchunk_seg;                               /* int32[max_chunks]  */
   int64_t total;
 } mux_plan_layout;
 

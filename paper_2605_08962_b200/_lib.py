@@ -28,16 +28,16 @@ class PlanCfg(C.Structure):
         "S", "n_carry", "n_carry_seqs", "n_chunks", "capacity", "gbs", "dp", "sp", "world",
         "mbs", "method", "pooled", "me", "mode")] + [
         ("row_bytes_in", C.c_int32 * N_GROUPS), ("row_bytes_ret", C.c_int32 * N_GROUPS),
-        ("chunk_bytes", C.c_int32), ("max_chunks", C.c_int32)]
+        ("chunk_bytes", C.c_int32)]
 
 
 LAYOUT_FIELDS = (
-    "header", "seq", "off", "span", "origin", "origin_pos", "group", "enc", "arena_off",
-    "enc_off", "llm_rank", "llm_row", "bin_fill", "bin_nspan", "bin_of", "chunk_nbins", "fills",
-    "nspans", "cu", "shard_len", "shard_start", "row_base", "arena_rows", "recv_rows",
-    "llm_rows", "order", "scratch_a", "scratch_b", "dseg_src_row", "dseg_dst_row", "dseg_rows",
-    "dseg_group", "dseg_dst_rank", "dseg_chunk0", "dchunk_seg", "rseg_src_row", "rseg_dst_row",
-    "rseg_rows", "rseg_group", "rseg_dst_rank", "rseg_chunk0", "rchunk_seg", "total")
+    "header", "sync", "seq", "off", "span", "origin", "origin_pos", "group", "enc", "arena_off",
+    "enc_off", "llm_rank", "llm_row", "bin_fill", "bin_nspan", "bin_of", "chunk_nbins",
+    "chunk_err", "fills", "nspans", "cu", "shard_len", "shard_start", "row_base", "arena_rows",
+    "recv_rows", "llm_rows", "order", "scratch_a", "scratch_b", "dseg_src_row", "dseg_dst_row",
+    "dseg_rows", "dseg_group", "dseg_dst_rank", "dseg_chunk0", "rseg_src_row", "rseg_dst_row",
+    "rseg_rows", "rseg_group", "rseg_dst_rank", "rseg_chunk0", "total")
 
 
 class PlanLayout(C.Structure):

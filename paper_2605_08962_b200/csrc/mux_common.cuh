@@ -108,16 +108,17 @@ __host__ __device__ __forceinline__ int group_of_mod(int m) {
 // Typed view of the plan blob.
 struct Plan {
   int64_t* hdr;
+  uint32_t* ticket;  // last-CTA ticket of plan_kernel (zero between launches)
   int32_t *seq, *off, *span, *origin, *origin_pos, *group, *enc, *llm_rank;
   int64_t *arena_off, *enc_off, *llm_row;
-  int32_t *bin_fill, *bin_nspan, *bin_of, *chunk_nbins, *fills, *nspans, *cu;
+  int32_t *bin_fill, *bin_nspan, *bin_of, *chunk_nbins, *chunk_err, *fills, *nspans, *cu;
   int32_t *shard_len, *shard_start;
   int64_t *row_base, *arena_rows, *recv_rows, *llm_rows;
   int32_t *order, *scratch_a, *scratch_b;
   int64_t *dsrc, *ddst, *drows, *dchunk0;
-  int32_t *dgroup, *drank, *dchunk_seg;
+  int32_t *dgroup, *drank;
   int64_t *rsrc, *rdst, *rrows, *rchunk0;
-  int32_t *rgroup, *rrank, *rchunk_seg;
+  int32_t *rgroup, *rrank;
 };
 
 Plan make_plan(void* base, const mux_plan_layout& L);

@@ -1,17 +1,21 @@
 // Device planner for one step of the encoder<->LLM data path (sm_100a).
 //
-// K_ffd      one CTA per drawn chunk: bitonic sort by (-len, id, index) and a
-//            warp-synchronous first fit over the bins
-//            (reference: pkg/src/muxsim/workload.py:240-262).
-// K_finalize one CTA: carry spans, global sequence ids, error checks
-//            (workload.py:245-248, :269-275), batch slice + replica owner
-//            (:265-280, :177-180), Ulysses shard geometry,
-//            origin / loader-arena / encoder assignment (LPT or KK;
-//            SPEC.md:390-407), encoder order, return pieces and the
-//            per-rank segment tables consumed by the copy kernels.
-// Everything is integer (or exact double) arithmetic, deterministic and
-// identical on every rank, so every rank can plan the whole step locally and
-// push its rows without exchanging counts.
+// One launch, `plan_kernel`, grid = one CTA per drawn chunk:
+//  part 1  every CTA packs its chunk: bitonic sort by (-len, id, index) in
+//          shared memory, then a warp-synchronous first fit with the bins in
+//          registers (reference: pkg/src/muxsim/workload.py:240-262);
+//  part 2  the last CTA to finish (atomic ticket) finalises the whole step:
+//          carry spans, global sequence ids, errors in the reference's order
+//          (workload.py:245-248, :269-275), batch slice and replica owner
+//          (:265-280, :177-180), Ulysses shard geometry,
+//          origins, loader-arena offsets, encoder assignment per pool (LPT or
+//          KK), encoder order, return pieces and the
+//          segment tables of rank `me` that drive the copy kernels.
+// For steps of up to kSmallS samples every per-sample array of part 2 lives
+// in shared memory (written back once at the end); larger steps work on the
+// plan blob in global memory.  Integer / exact-double arithmetic only, so
+// every rank computes the identical plan and pushes rows without exchanging
+// counts.
 
 #include <climits>
 #include <cstdarg>
@@ -21,6 +25,12 @@
 #include "mux_common.cuh"
 
 namespace mux {
+
+constexpr int kSmallS = 1024;   // per-sample state in shared memory up to this S
+constexpr int kThreads = 1024;
+constexpr int kRegSlots = 8;    // first-fit bins in registers: 32 lanes x 8 = 256
+constexpr int kKkMax = 512;     // KK pool limit (one warp, tuples in shared memory)
+constexpr int kMaxChunks = 1024;
 
 // --------------------------------------------------------------------------
 // layout
@@ -33,6 +43,10 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   }
   if (c.S > 4096) {
     set_error("step table of %d samples exceeds the device planner limit 4096", c.S);
+    return MUX_ERR_VALUE;
+  }
+  if (c.n_chunks > kMaxChunks) {
+    set_error("more than %d chunks in one step", kMaxChunks);
     return MUX_ERR_VALUE;
   }
   if (c.mode == MUX_MODE_STEP) {
@@ -51,7 +65,6 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   const int64_t gb = (c.gbs > 0 ? c.gbs : 1) * (c.sp > 0 ? c.sp : 1);
   const int64_t W = (c.world > 0 ? c.world : 1);
   const int64_t R = max_ret_of(c);
-  const int64_t MC = c.max_chunks > 0 ? c.max_chunks : 1;
   int64_t o = 0;
   auto take = [&](int64_t bytes) {
     int64_t at = o;
@@ -59,6 +72,7 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
     return at;
   };
   L->header = take(8 * MUX_H_SLOTS);
+  L->sync = take(8);
   L->seq = take(4 * S);
   L->off = take(4 * S);
   L->span = take(4 * S);
@@ -74,6 +88,7 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->bin_nspan = take(4 * S);
   L->bin_of = take(4 * S);
   L->chunk_nbins = take(4 * nch);
+  L->chunk_err = take(4 * nch);
   L->fills = take(4 * mseq);
   L->nspans = take(4 * mseq);
   L->cu = take(4 * (gb + 1));
@@ -92,14 +107,12 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->dseg_group = take(4 * S);
   L->dseg_dst_rank = take(4 * S);
   L->dseg_chunk0 = take(8 * (S + 1));
-  L->dchunk_seg = take(4 * MC);
   L->rseg_src_row = take(8 * R);
   L->rseg_dst_row = take(8 * R);
   L->rseg_rows = take(8 * R);
   L->rseg_group = take(4 * R);
   L->rseg_dst_rank = take(4 * R);
   L->rseg_chunk0 = take(8 * (R + 1));
-  L->rchunk_seg = take(4 * MC);
   L->total = o;
   return MUX_OK;
 }
@@ -112,6 +125,7 @@ static T* at(void* base, int64_t off) {
 Plan make_plan(void* b, const mux_plan_layout& L) {
   Plan p;
   p.hdr = at<int64_t>(b, L.header);
+  p.ticket = at<uint32_t>(b, L.sync);
   p.seq = at<int32_t>(b, L.seq);
   p.off = at<int32_t>(b, L.off);
   p.span = at<int32_t>(b, L.span);
@@ -127,6 +141,7 @@ Plan make_plan(void* b, const mux_plan_layout& L) {
   p.bin_nspan = at<int32_t>(b, L.bin_nspan);
   p.bin_of = at<int32_t>(b, L.bin_of);
   p.chunk_nbins = at<int32_t>(b, L.chunk_nbins);
+  p.chunk_err = at<int32_t>(b, L.chunk_err);
   p.fills = at<int32_t>(b, L.fills);
   p.nspans = at<int32_t>(b, L.nspans);
   p.cu = at<int32_t>(b, L.cu);
@@ -145,14 +160,12 @@ Plan make_plan(void* b, const mux_plan_layout& L) {
   p.dgroup = at<int32_t>(b, L.dseg_group);
   p.drank = at<int32_t>(b, L.dseg_dst_rank);
   p.dchunk0 = at<int64_t>(b, L.dseg_chunk0);
-  p.dchunk_seg = at<int32_t>(b, L.dchunk_seg);
   p.rsrc = at<int64_t>(b, L.rseg_src_row);
   p.rdst = at<int64_t>(b, L.rseg_dst_row);
   p.rrows = at<int64_t>(b, L.rseg_rows);
   p.rgroup = at<int32_t>(b, L.rseg_group);
   p.rrank = at<int32_t>(b, L.rseg_dst_rank);
   p.rchunk0 = at<int64_t>(b, L.rseg_chunk0);
-  p.rchunk_seg = at<int32_t>(b, L.rchunk_seg);
   return p;
 }
 
@@ -160,18 +173,23 @@ Plan make_plan_const(const void* b, const mux_plan_layout& L) {
   return make_plan(const_cast<void*>(b), L);
 }
 
+// Phase timestamps (globaltimer, ns) in header slots 16..31 for profiling.
+__device__ __forceinline__ void stamp(Plan& p, int slot) {
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.hdr[slot] = (int64_t)t;
+  }
+}
+
 // --------------------------------------------------------------------------
-// K_ffd: first-fit decreasing of one chunk
+// sort keys, LPT and Karmarkar-Karp
 // --------------------------------------------------------------------------
 
-constexpr int kFfdThreads = 512;
-constexpr int kRegSlots = 8;  // bins kept in registers: 32 lanes x 8 = 256
-
-struct FfdKey {
+struct FfdKey {  // (-len, id, index) ascending; padding (>= n) last
   const int32_t* len;
   const int64_t* id;
   int n;
-  // (-len, id, index) ascending; padding (>= n) last.  Stable == index tie.
   __device__ bool operator()(int a, int b) const {
     if (a >= n) return false;
     if (b >= n) return true;
@@ -181,21 +199,248 @@ struct FfdKey {
   }
 };
 
-__global__ void __launch_bounds__(kFfdThreads) ffd_kernel(mux_plan_cfg cfg, const int32_t* lens,
-                                                          const int64_t* ids,
-                                                          const int32_t* chunk_off, Plan p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int64_t s_warp[33];
+struct PoolKey {  // (pool, -cost, id, table index) ascending; padding last
+  const int32_t* pool;
+  const double* cost;
+  const int64_t* id;
+  const int32_t* tidx;
+  int n;
+  __device__ bool operator()(int a, int b) const {
+    if (a >= n) return false;
+    if (b >= n) return true;
+    if (pool[a] != pool[b]) return pool[a] < pool[b];
+    if (cost[a] != cost[b]) return cost[a] > cost[b];
+    if (id[a] != id[b]) return id[a] < id[b];
+    return tidx[a] < tidx[b];
+  }
+};
+
+// Sequential LPT over sorted items by one warp; out[k] = rank of item k.
+__device__ void lpt_warp(const int* s_ord, const double* cost, int n, int g, int32_t* out_rank) {
+  const int lane = threadIdx.x & 31;
+  double load = 0.0;
+  int nxt = n > 0 ? s_ord[0] : 0;
+  double nc = n > 0 ? cost[nxt] : 0.0;
+  for (int q = 0; q < n; ++q) {
+    const int k = nxt;
+    const double c = nc;
+    if (q + 1 < n) {
+      nxt = s_ord[q + 1];
+      nc = cost[nxt];
+    }
+    double l = lane < g ? load : __longlong_as_double(0x7ff0000000000000LL);
+    int r = lane;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const double l2 = __shfl_xor_sync(MUX_FULL, l, o, 8);
+      const int r2 = __shfl_xor_sync(MUX_FULL, r, o, 8);
+      if (l2 < l || (l2 == l && r2 < r)) {
+        l = l2;
+        r = r2;
+      }
+    }
+    r = __shfl_sync(MUX_FULL, r, 0);
+    if (lane == r) load = __dadd_rn(load, c);
+    if (lane == 0) out_rank[k] = r;
+  }
+}
+
+struct KkSmem {
+  double sum[kKkMax * 8];
+  int32_t mn[kKkMax * 8];
+  int32_t head[kKkMax * 8];
+  int32_t tail[kKkMax * 8];
+  int32_t next[kKkMax];
+  int32_t alive[kKkMax];
+  double spread[kKkMax];
+  int32_t tmin[kKkMax];
+};
+
+__device__ __forceinline__ bool kk_better(double sa, int ma, double sb, int mb) {
+  return sa > sb || (sa == sb && ma < mb);
+}
+
+// Karmarkar-Karp, g-way largest differencing (pinned reading in
+// oracle/planner.py:kk_assign).  One warp; g <= 8; n <= kKkMax.
+// w[t] / out_rank[t] for t < n.
+__device__ void kk_warp(KkSmem& K, const double* w, int n, int g, int32_t* out_rank) {
+  const int lane = threadIdx.x & 31;
+  const int INF = INT_MAX;
+  for (int t = lane; t < n; t += 32) {
+    for (int j = 0; j < g; ++j) {
+      K.sum[t * 8 + j] = j == 0 ? w[t] : 0.0;
+      K.mn[t * 8 + j] = j == 0 ? t : INF;
+      K.head[t * 8 + j] = j == 0 ? t : -1;
+      K.tail[t * 8 + j] = j == 0 ? t : -1;
+    }
+    K.next[t] = -1;
+    K.alive[t] = t;
+    K.spread[t] = g > 1 ? w[t] : 0.0;
+    K.tmin[t] = t;
+  }
+  __syncwarp();
+  int na = n;
+  while (na > 1) {
+    int a = -1, b = -1;  // top-2 by (spread desc, tmin asc) over the alive list
+    for (int pass = 0; pass < 2; ++pass) {
+      double bs = -1.0;
+      int bm = INF, bp = -1;
+      for (int x = lane; x < na; x += 32) {
+        const int t = K.alive[x];
+        if (t == a) continue;
+        if (bp < 0 || kk_better(K.spread[t], K.tmin[t], bs, bm)) {
+          bs = K.spread[t];
+          bm = K.tmin[t];
+          bp = x;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double s2 = __shfl_xor_sync(MUX_FULL, bs, o);
+        const int m2 = __shfl_xor_sync(MUX_FULL, bm, o);
+        const int p2 = __shfl_xor_sync(MUX_FULL, bp, o);
+        if (p2 >= 0 && (bp < 0 || kk_better(s2, m2, bs, bm))) {
+          bs = s2;
+          bm = m2;
+          bp = p2;
+        }
+      }
+      if (pass == 0) a = K.alive[bp];
+      else b = bp;  // position of b in the alive list
+    }
+    const int tb = K.alive[b];
+    double sA = 0, sB = 0;  // lane j < g owns subset j of A and of B
+    int mA = INF, mB = INF, hA = -1, tA = -1, hB = -1, tB = -1;
+    if (lane < g) {
+      sA = K.sum[a * 8 + lane]; mA = K.mn[a * 8 + lane];
+      hA = K.head[a * 8 + lane]; tA = K.tail[a * 8 + lane];
+      sB = K.sum[tb * 8 + lane]; mB = K.mn[tb * 8 + lane];
+      hB = K.head[tb * 8 + lane]; tB = K.tail[tb * 8 + lane];
+    }
+    // rank of my A subset in (sum desc, mn asc), of my B subset in (sum asc, mn asc);
+    // identical (empty) subsets tie-break by lane
+    int rA = 0, rB = 0;
+    for (int j = 0; j < g; ++j) {
+      const double sAj = __shfl_sync(MUX_FULL, sA, j), sBj = __shfl_sync(MUX_FULL, sB, j);
+      const int mAj = __shfl_sync(MUX_FULL, mA, j), mBj = __shfl_sync(MUX_FULL, mB, j);
+      if (lane < g && j != lane) {
+        if (sAj > sA || (sAj == sA && (mAj < mA || (mAj == mA && j < lane)))) ++rA;
+        if (sBj < sB || (sBj == sB && (mBj < mB || (mBj == mB && j < lane)))) ++rB;
+      }
+    }
+    __syncwarp();
+    if (lane < g) {  // A subsets to slot rA of tuple a, B subsets to slot rB of tuple tb
+      K.sum[a * 8 + rA] = sA; K.mn[a * 8 + rA] = mA;
+      K.head[a * 8 + rA] = hA; K.tail[a * 8 + rA] = tA;
+      K.sum[tb * 8 + rB] = sB; K.mn[tb * 8 + rB] = mB;
+      K.head[tb * 8 + rB] = hB; K.tail[tb * 8 + rB] = tB;
+    }
+    __syncwarp();
+    if (lane < g) {  // pair A's j-th largest with B's j-th smallest
+      const int j = lane;
+      const double s = __dadd_rn(K.sum[a * 8 + j], K.sum[tb * 8 + j]);
+      const int m1 = K.mn[a * 8 + j], m2 = K.mn[tb * 8 + j];
+      int h1 = K.head[a * 8 + j], t1 = K.tail[a * 8 + j];
+      const int h2 = K.head[tb * 8 + j], t2 = K.tail[tb * 8 + j];
+      if (h1 < 0) { h1 = h2; t1 = t2; }
+      else if (h2 >= 0) { K.next[t1] = h2; t1 = t2; }
+      K.sum[a * 8 + j] = s;
+      K.mn[a * 8 + j] = m1 < m2 ? m1 : m2;
+      K.head[a * 8 + j] = h1;
+      K.tail[a * 8 + j] = t1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double mx = K.sum[a * 8], mi = K.sum[a * 8];
+      int tm = K.mn[a * 8];
+      for (int j = 1; j < g; ++j) {
+        const double s = K.sum[a * 8 + j];
+        mx = s > mx ? s : mx;
+        mi = s < mi ? s : mi;
+        tm = K.mn[a * 8 + j] < tm ? K.mn[a * 8 + j] : tm;
+      }
+      K.spread[a] = __dsub_rn(mx, mi);
+      K.tmin[a] = tm;
+      K.alive[b] = K.alive[na - 1];
+    }
+    --na;
+    __syncwarp();
+  }
+  const int f = K.alive[0];  // final subsets -> ranks by (sum desc, mn asc)
+  double s = 0;
+  int m = INF, h = -1;
+  if (lane < g) { s = K.sum[f * 8 + lane]; m = K.mn[f * 8 + lane]; h = K.head[f * 8 + lane]; }
+  int r = 0;
+  for (int j = 0; j < g; ++j) {
+    const double sj = __shfl_sync(MUX_FULL, s, j);
+    const int mj = __shfl_sync(MUX_FULL, m, j);
+    if (lane < g && j != lane && (sj > s || (sj == s && (mj < m || (mj == m && j < lane))))) ++r;
+  }
+  if (lane < g)
+    for (int t = h; t >= 0; t = K.next[t]) out_rank[t] = r;
+  __syncwarp();
+}
+
+// --------------------------------------------------------------------------
+// block-wide multi-key scan: one element per thread per call, K <= 16 keys.
+// Returns the exclusive prefix of `val` among earlier elements (this call
+// and previous calls) with the same key; s_carry[k] accumulates per-key
+// totals across calls (caller zeroes it).  Three barriers per call.
+// --------------------------------------------------------------------------
+constexpr int kMaxKeys = 16;
+
+__device__ __forceinline__ int64_t multi_scan(int key, int64_t val, int K, int64_t* s_wk,
+                                              int64_t* s_carry) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t mine_incl = 0;
+#pragma unroll
+  for (int k = 0; k < kMaxKeys; ++k) {
+    if (k >= K) break;
+    int64_t x = key == k ? val : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(MUX_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wk[w * kMaxKeys + k] = x;
+    if (key == k) mine_incl = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int k = threadIdx.x;
+    int64_t run = s_carry[k];
+    for (int j = 0; j < nw; ++j) {
+      const int64_t t = s_wk[j * kMaxKeys + k];
+      s_wk[j * kMaxKeys + k] = run;
+      run += t;
+    }
+    s_carry[k] = run;
+  }
+  __syncthreads();
+  const int64_t r = (key >= 0 && key < K) ? s_wk[w * kMaxKeys + key] + mine_incl - val : 0;
+  __syncthreads();
+  return r;
+}
+
+// --------------------------------------------------------------------------
+// part 1: first-fit decreasing of one chunk (whole CTA sorts; warp 0 places)
+// --------------------------------------------------------------------------
+
+__device__ void ffd_chunk(const mux_plan_cfg& cfg, const int32_t* lens, const int64_t* ids,
+                          const int32_t* chunk_off, Plan& p, unsigned char* smem,
+                          int64_t* s_warp) {
+  __shared__ int s_err;
   const int c = blockIdx.x;
   const int lo = chunk_off[c], n = chunk_off[c + 1] - lo;
   const int npad = next_pow2(n > 0 ? n : 1);
   int64_t* s_id = reinterpret_cast<int64_t*>(smem);
   int32_t* s_len = reinterpret_cast<int32_t*>(s_id + npad);
   int32_t* s_ord = s_len + npad;
-  int32_t* s_fill = s_ord + npad;   // smem first-fit path only
+  int32_t* s_fill = s_ord + npad;  // shared-memory first fit (many bins) only
   int32_t* s_nsp = s_fill + npad;
   const int cap = cfg.capacity;
-
+  if (threadIdx.x == 0) s_err = INT_MAX;
+  __syncthreads();
   int64_t my_total = 0;
   for (int i = threadIdx.x; i < npad; i += blockDim.x) {
     if (i < n) {
@@ -203,17 +448,16 @@ __global__ void __launch_bounds__(kFfdThreads) ffd_kernel(mux_plan_cfg cfg, cons
       s_len[i] = L;
       s_id[i] = ids[lo + i];
       my_total += L;
-      if (L > cap)  // first offender in table order wins (workload.py:245-248)
-        atomicMin(reinterpret_cast<unsigned long long*>(&p.hdr[MUX_H_ERR_INDEX]),
-                  (unsigned long long)(lo + i));
+      if (L > cap) atomicMin(&s_err, lo + i);  // first offender in table order
     }
     s_ord[i] = i;
   }
   int64_t total;
-  block_excl_scan(my_total, &total, s_warp);
+  block_excl_scan(my_total, &total, s_warp);  // (its barriers also publish the loads)
   bitonic_sort(s_ord, npad, FfdKey{s_len, s_id, n});
+  if (threadIdx.x == 0) p.chunk_err[c] = s_err;
 
-  // FF never leaves two bins at most half full, so #bins <= 2*total/cap + 1.
+  // first fit never leaves two bins at most half full: #bins <= 2*total/cap + 1
   const int64_t bound = cap > 0 ? 2 * total / cap + 2 : n;
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
@@ -298,245 +542,143 @@ __global__ void __launch_bounds__(kFfdThreads) ffd_kernel(mux_plan_cfg cfg, cons
 }
 
 // --------------------------------------------------------------------------
-// assignment: LPT and Karmarkar-Karp over a pool held in shared memory
+// part 2: finalise (one CTA)
 // --------------------------------------------------------------------------
 
-struct LptKey {
-  const double* cost;
-  const int64_t* id;
-  const int32_t* tidx;
-  int n;
-  __device__ bool operator()(int a, int b) const {
-    if (a >= n) return false;
-    if (b >= n) return true;
-    if (cost[a] != cost[b]) return cost[a] > cost[b];
-    if (id[a] != id[b]) return id[a] < id[b];
-    return tidx[a] < tidx[b];
-  }
+struct Work {  // per-sample working arrays: shared memory (S <= kSmallS) or the plan blob
+  int32_t *len, *seq, *off, *span, *grp, *org, *k, *opos, *enc, *within, *order;
+  int64_t *id, *aoff, *eoff;
+  int32_t *fills, *nspans;
 };
 
-// Sequential LPT over sorted items by one warp; out[k] = rank of item k.
-__device__ void lpt_warp(const int* s_ord, const double* cost, int n, int g, int32_t* out_rank) {
-  const int lane = threadIdx.x & 31;
-  double load = 0.0;
-  for (int q = 0; q < n; ++q) {
-    const int k = s_ord[q];
-    const double c = cost[k];
-    double l = lane < g ? load : __longlong_as_double(0x7ff0000000000000LL);
-    int r = lane;
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      const double l2 = __shfl_xor_sync(MUX_FULL, l, o, 8);
-      const int r2 = __shfl_xor_sync(MUX_FULL, r, o, 8);
-      if (l2 < l || (l2 == l && r2 < r)) {
-        l = l2;
-        r = r2;
-      }
-    }
-    r = __shfl_sync(MUX_FULL, r, 0);
-    if (lane == r) load = __dadd_rn(load, c);
-    if (lane == 0) out_rank[k] = r;
-  }
-}
-
-// Karmarkar-Karp, g-way largest differencing (pinned reading in
-// oracle/planner.py:kk_assign).  One warp; g <= 8; n <= kKkMax.
-constexpr int kKkMax = 512;
-
-struct KkSmem {
-  double sum[kKkMax * 8];
-  int32_t mn[kKkMax * 8];
-  int32_t head[kKkMax * 8];
-  int32_t tail[kKkMax * 8];
-  int32_t next[kKkMax];
-  int32_t alive[kKkMax];
-  double spread[kKkMax];
-  int32_t tmin[kKkMax];
+struct SmemPlan {  // byte offsets of the finalize-phase shared-memory regions
+  int work, shard, lpt, kk, total;
 };
 
-__device__ __forceinline__ bool kk_better(double sa, int ma, double sb, int mb) {
-  return sa > sb || (sa == sb && ma < mb);
+__host__ __device__ inline SmemPlan smem_plan(int S, int n_seq_max, int gb, int method) {
+  SmemPlan L;
+  int o = 0;
+  L.work = o;
+  if (S <= kSmallS) o += 68 * S + 8 * n_seq_max;
+  o = (int)align_up(o, 16);
+  L.shard = o;  // shard start / length per (sequence, shard), phases D..I
+  o += 8 * gb;
+  o = (int)align_up(o, 16);
+  L.lpt = o;  // phase E counters, then the pool sort (phase G)
+  int spad = 1;
+  while (spad < S) spad <<= 1;
+  o += 32 * spad > 8 * gb ? 32 * spad : 8 * gb;  // cost f64, id i64, tidx, pool, ord, rank
+  o = (int)align_up(o, 16);
+  L.kk = o;
+  if (method == MUX_KK) o += (int)sizeof(KkSmem);
+  L.total = o;
+  return L;
 }
-
-__device__ void kk_warp(KkSmem& K, const double* w, int n, int g, int32_t* out_rank) {
-  const int lane = threadIdx.x & 31;
-  const int INF = INT_MAX;
-  for (int t = lane; t < n; t += 32) {
-    for (int j = 0; j < g; ++j) {
-      K.sum[t * 8 + j] = j == 0 ? w[t] : 0.0;
-      K.mn[t * 8 + j] = j == 0 ? t : INF;
-      K.head[t * 8 + j] = j == 0 ? t : -1;
-      K.tail[t * 8 + j] = j == 0 ? t : -1;
-    }
-    K.next[t] = -1;
-    K.alive[t] = t;
-    K.spread[t] = g > 1 ? w[t] : 0.0;
-    K.tmin[t] = t;
-  }
-  __syncwarp();
-  int na = n;
-  while (na > 1) {
-    // top-2 by (spread desc, tmin asc) over the alive list
-    int a = -1, b = -1;
-    for (int pass = 0; pass < 2; ++pass) {
-      double bs = -1.0;
-      int bm = INF, bp = -1;
-      for (int x = lane; x < na; x += 32) {
-        const int t = K.alive[x];
-        if (t == a) continue;
-        if (bp < 0 || kk_better(K.spread[t], K.tmin[t], bs, bm)) {
-          bs = K.spread[t];
-          bm = K.tmin[t];
-          bp = x;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double s2 = __shfl_xor_sync(MUX_FULL, bs, o);
-        const int m2 = __shfl_xor_sync(MUX_FULL, bm, o);
-        const int p2 = __shfl_xor_sync(MUX_FULL, bp, o);
-        if (p2 >= 0 && (bp < 0 || kk_better(s2, m2, bs, bm))) {
-          bs = s2;
-          bm = m2;
-          bp = p2;
-        }
-      }
-      if (pass == 0) a = K.alive[bp];
-      else b = bp;  // position of b in the alive list
-    }
-    const int tb = K.alive[b];
-    // lane j < g owns subset j of A and of B
-    double sA = 0, sB = 0;
-    int mA = INF, mB = INF, hA = -1, tA = -1, hB = -1, tB = -1;
-    if (lane < g) {
-      sA = K.sum[a * 8 + lane]; mA = K.mn[a * 8 + lane];
-      hA = K.head[a * 8 + lane]; tA = K.tail[a * 8 + lane];
-      sB = K.sum[tb * 8 + lane]; mB = K.mn[tb * 8 + lane];
-      hB = K.head[tb * 8 + lane]; tB = K.tail[tb * 8 + lane];
-    }
-    // rank of my A subset in (sum desc, mn asc), of my B subset in (sum asc, mn asc)
-    int rA = 0, rB = 0;
-    for (int j = 0; j < g; ++j) {
-      const double sAj = __shfl_sync(MUX_FULL, sA, j), sBj = __shfl_sync(MUX_FULL, sB, j);
-      const int mAj = __shfl_sync(MUX_FULL, mA, j), mBj = __shfl_sync(MUX_FULL, mB, j);
-      if (lane < g && j != lane) {
-        if (sAj > sA || (sAj == sA && (mAj < mA || (mAj == mA && j < lane)))) ++rA;
-        if (sBj < sB || (sBj == sB && (mBj < mB || (mBj == mB && j < lane)))) ++rB;
-      }
-    }
-    __syncwarp();
-    // scatter A subsets to slot rA (tuple a), then pair with the B subset of rank rA
-    if (lane < g) {
-      K.sum[a * 8 + rA] = sA; K.mn[a * 8 + rA] = mA;
-      K.head[a * 8 + rA] = hA; K.tail[a * 8 + rA] = tA;
-    }
-    __syncwarp();
-    // stash B subsets by rank in tuple tb's slots (tb is dead after this merge)
-    if (lane < g) {
-      K.sum[tb * 8 + rB] = sB; K.mn[tb * 8 + rB] = mB;
-      K.head[tb * 8 + rB] = hB; K.tail[tb * 8 + rB] = tB;
-    }
-    __syncwarp();
-    if (lane < g) {
-      const int j = lane;
-      const double s = __dadd_rn(K.sum[a * 8 + j], K.sum[tb * 8 + j]);
-      const int m1 = K.mn[a * 8 + j], m2 = K.mn[tb * 8 + j];
-      int h1 = K.head[a * 8 + j], t1 = K.tail[a * 8 + j];
-      const int h2 = K.head[tb * 8 + j], t2 = K.tail[tb * 8 + j];
-      if (h1 < 0) { h1 = h2; t1 = t2; }
-      else if (h2 >= 0) { K.next[t1] = h2; t1 = t2; }
-      K.sum[a * 8 + j] = s;
-      K.mn[a * 8 + j] = m1 < m2 ? m1 : m2;
-      K.head[a * 8 + j] = h1;
-      K.tail[a * 8 + j] = t1;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      double mx = K.sum[a * 8], mi = K.sum[a * 8];
-      int tm = K.mn[a * 8];
-      for (int j = 1; j < g; ++j) {
-        const double s = K.sum[a * 8 + j];
-        mx = s > mx ? s : mx;
-        mi = s < mi ? s : mi;
-        tm = K.mn[a * 8 + j] < tm ? K.mn[a * 8 + j] : tm;
-      }
-      K.spread[a] = __dsub_rn(mx, mi);
-      K.tmin[a] = tm;
-      K.alive[b] = K.alive[na - 1];
-    }
-    --na;
-    __syncwarp();
-  }
-  // final subsets -> ranks by (sum desc, mn asc)
-  const int f = K.alive[0];
-  double s = 0;
-  int m = INF, h = -1;
-  if (lane < g) { s = K.sum[f * 8 + lane]; m = K.mn[f * 8 + lane]; h = K.head[f * 8 + lane]; }
-  int r = 0;
-  for (int j = 0; j < g; ++j) {
-    const double sj = __shfl_sync(MUX_FULL, s, j);
-    const int mj = __shfl_sync(MUX_FULL, m, j);
-    if (lane < g && j != lane && (sj > s || (sj == s && (mj < m || (mj == m && j < lane))))) ++r;
-  }
-  if (lane < g)
-    for (int t = h; t >= 0; t = K.next[t]) out_rank[t] = r;
-  __syncwarp();
-}
-
-// --------------------------------------------------------------------------
-// K_finalize
-// --------------------------------------------------------------------------
-
-constexpr int kFinThreads = 1024;
-
-struct LptSmem {
-  double cost[4096];
-  int64_t id[4096];
-  int32_t tidx[4096];
-  int32_t ord[4096];
-  int32_t rank[4096];
-};
 
 __device__ __forceinline__ void set_status(Plan& p, int st) {
   if (threadIdx.x == 0) p.hdr[MUX_H_STATUS] = st;
 }
 
-__global__ void __launch_bounds__(kFinThreads) finalize_kernel(mux_plan_cfg cfg,
-                                                               const int32_t* lens,
-                                                               const int32_t* mods,
-                                                               const int64_t* ids,
-                                                               const int32_t* carry_seq,
-                                                               const int32_t* chunk_off, Plan p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int64_t s_warp[33];
-  __shared__ int64_t s_tot[64];
-  __shared__ int32_t s_chbase[1025];
-  __shared__ int32_t s_nseq;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int S = cfg.S, nc = cfg.n_carry, nch = cfg.n_chunks;
+// write the shared-memory working arrays back to the plan blob
+__device__ void emit(const mux_plan_cfg& cfg, Plan& p, const Work& w, bool small, int n_seq,
+                     bool full) {
+  if (!small) return;
+  for (int i = threadIdx.x; i < cfg.S; i += blockDim.x) {
+    p.seq[i] = w.seq[i];
+    p.off[i] = w.off[i];
+    p.span[i] = w.span[i];
+    if (full) {
+      p.group[i] = w.grp[i];
+      p.origin[i] = w.org[i];
+      p.origin_pos[i] = w.opos[i];
+      p.enc[i] = w.enc[i];
+      p.arena_off[i] = w.aoff[i];
+      p.enc_off[i] = w.eoff[i];
+    }
+  }
+  for (int q = threadIdx.x; q < n_seq; q += blockDim.x) {
+    p.fills[q] = w.fills[q];
+    p.nspans[q] = w.nspans[q];
+  }
+}
 
-  // ---- A. chunk sequence bases -----------------------------------------
+__device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int32_t* mods,
+                         const int64_t* ids, const int32_t* carry_seq, const int32_t* chunk_off,
+                         Plan& p, unsigned char* smem, int64_t* s_warp) {
+  __shared__ int64_t s_wk[32 * kMaxKeys];
+  __shared__ int64_t s_carry[kMaxKeys];
+  __shared__ int32_t s_chbase[kMaxChunks + 1];
+  __shared__ int32_t s_misc[4];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int S = cfg.S, nc = cfg.n_carry, nch = cfg.n_chunks, W = cfg.world;
+  const int max_seq = cfg.n_carry_seqs + (S - nc) + 1;
+  const bool small = S <= kSmallS;
+  const SmemPlan SL = smem_plan(S, max_seq, cfg.gbs * cfg.sp, cfg.method);
+  stamp(p, 17);
+
+  // ---- working storage -----------------------------------------------------
+  Work w;
+  if (small) {
+    unsigned char* b = smem + SL.work;
+    w.id = reinterpret_cast<int64_t*>(b);
+    w.aoff = w.id + S;
+    w.eoff = w.aoff + S;
+    int32_t* q = reinterpret_cast<int32_t*>(w.eoff + S);
+    w.len = q; q += S;
+    w.seq = q; q += S;
+    w.off = q; q += S;
+    w.span = q; q += S;
+    w.grp = q; q += S;
+    w.org = q; q += S;
+    w.k = q; q += S;
+    w.opos = q; q += S;
+    w.enc = q; q += S;
+    w.within = q; q += S;
+    w.order = q; q += S;
+    w.fills = q; q += max_seq;
+    w.nspans = q;
+    for (int i = tid; i < S; i += nt) {
+      w.len[i] = lens[i];
+      w.id[i] = ids[i];
+    }
+  } else {
+    w.len = const_cast<int32_t*>(lens);
+    w.id = const_cast<int64_t*>(ids);
+    w.seq = p.seq; w.off = p.off; w.span = p.span; w.grp = p.group; w.org = p.origin;
+    w.k = p.scratch_a; w.opos = p.origin_pos; w.enc = p.enc; w.within = p.scratch_b;
+    w.order = p.order; w.aoff = p.arena_off; w.eoff = p.enc_off;
+    w.fills = p.fills; w.nspans = p.nspans;
+  }
+
+  // ---- A. chunk sequence bases, first oversize sample ------------------------
   if (tid == 0) {
-    int b = cfg.n_carry_seqs;
+    int b = cfg.n_carry_seqs, err = INT_MAX;
     for (int c = 0; c < nch; ++c) {
       s_chbase[c] = b;
-      b += p.chunk_nbins[c];
+      b += __ldcg(p.chunk_nbins + c);
+      const int e = __ldcg(p.chunk_err + c);
+      err = e < err ? e : err;
     }
     s_chbase[nch] = b;
-    s_nseq = b;
+    s_misc[0] = b;    // n_seq
+    s_misc[1] = err;  // first oversize table index
   }
-  for (int q = tid; q < cfg.n_carry_seqs; q += nt) p.fills[q] = p.nspans[q] = 0;
+  for (int q = tid; q < cfg.n_carry_seqs; q += nt) w.fills[q] = w.nspans[q] = 0;
   __syncthreads();
-  const int n_seq = s_nseq;
+  const int n_seq = s_misc[0];
 
-  // ---- B. global sequence ids, carry offsets, fills ----------------------
+  // ---- B. global sequence ids, carry spans, fills -----------------------------
   for (int c = 0; c < nch; ++c) {
     const int lo = chunk_off[c], hi = chunk_off[c + 1];
-    const int nb = p.chunk_nbins[c];
-    for (int i = lo + tid; i < hi; i += nt) p.seq[i] = s_chbase[c] + p.bin_of[i];
+    const int base = s_chbase[c], nb = s_chbase[c + 1] - base;
+    for (int i = lo + tid; i < hi; i += nt) {
+      w.seq[i] = base + __ldcg(p.bin_of + i);
+      w.off[i] = __ldcg(p.off + i);
+      w.span[i] = __ldcg(p.span + i);
+    }
     for (int b = tid; b < nb; b += nt) {
-      p.fills[s_chbase[c] + b] = p.bin_fill[lo + b];
-      p.nspans[s_chbase[c] + b] = p.bin_nspan[lo + b];
+      w.fills[base + b] = __ldcg(p.bin_fill + lo + b);
+      w.nspans[base + b] = __ldcg(p.bin_nspan + lo + b);
     }
   }
   __syncthreads();
@@ -544,126 +686,124 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(mux_plan_cfg cfg,
     const int q = carry_seq[i];
     int o = 0, sp = 0;
     for (int j = i - 1; j >= 0 && carry_seq[j] == q; --j) {
-      o += lens[j];
+      o += w.len[j];
       ++sp;
     }
-    p.seq[i] = q;
-    p.off[i] = o;
-    p.span[i] = sp;
+    w.seq[i] = q;
+    w.off[i] = o;
+    w.span[i] = sp;
     if (i + 1 == nc || carry_seq[i + 1] != q) {
-      p.fills[q] = o + lens[i];
-      p.nspans[q] = sp + 1;
+      w.fills[q] = o + w.len[i];
+      w.nspans[q] = sp + 1;
     }
   }
   __syncthreads();
 
-  // ---- C. errors in the reference's order --------------------------------
-  if (tid == 0) p.hdr[MUX_H_N_SEQ] = n_seq;
-  const int64_t err_idx = p.hdr[MUX_H_ERR_INDEX];
-  if (err_idx >= 0) {
-    set_status(p, MUX_ERR_PACKING);
-    return;
+  // ---- C. errors in the reference's order ------------------------------------
+  stamp(p, 18);
+  const int err_idx = s_misc[1];
+  if (tid == 0) {
+    p.hdr[MUX_H_N_SEQ] = n_seq;
+    p.hdr[MUX_H_ERR_INDEX] = err_idx == INT_MAX ? -1 : err_idx;
   }
-  if (cfg.mode == MUX_MODE_PACK) {
-    set_status(p, MUX_OK);
-    return;
-  }
-  if (cfg.gbs % (cfg.dp * cfg.mbs) != 0 || cfg.dp * cfg.sp != cfg.world) {
-    set_status(p, MUX_ERR_CONFIG);
-    return;
-  }
-  if (n_seq < cfg.gbs) {
-    set_status(p, MUX_ERR_VALUE);
+  int early = -1;
+  if (err_idx != INT_MAX) early = MUX_ERR_PACKING;
+  else if (cfg.mode == MUX_MODE_PACK) early = MUX_OK;
+  else if (cfg.gbs % (cfg.dp * cfg.mbs) != 0 || cfg.dp * cfg.sp != cfg.world)
+    early = MUX_ERR_CONFIG;
+  else if (n_seq < cfg.gbs) early = MUX_ERR_VALUE;
+  if (early >= 0) {
+    emit(cfg, p, w, small, n_seq, false);
+    __syncthreads();
+    set_status(p, early);
     return;
   }
 
-  // ---- D. batch geometry ----------------------------------------------------
-  const int gbs = cfg.gbs, sp = cfg.sp, W = cfg.world, P = gbs / cfg.dp;
+  // ---- D. batch geometry: cu_seqlens, Ulysses shards, per-rank row bases ------
+  stamp(p, 19);
+  const int gbs = cfg.gbs, sp = cfg.sp, P = gbs / cfg.dp;
   {
     int64_t carry = 0;
     for (int base = 0; base < gbs; base += nt) {
       const int q = base + tid;
-      const int64_t v = q < gbs ? p.fills[q] : 0;
       int64_t tot;
-      const int64_t pre = block_excl_scan(v, &tot, s_warp);
+      const int64_t pre = block_excl_scan(q < gbs ? w.fills[q] : 0, &tot, s_warp);
       if (q < gbs) p.cu[q] = (int32_t)(carry + pre);
       carry += tot;
     }
     if (tid == 0) p.cu[gbs] = (int32_t)carry;
   }
+  int32_t* s_sstart = reinterpret_cast<int32_t*>(smem + SL.shard);  // [gbs*sp], D..I
+  int32_t* s_slen = s_sstart + gbs * sp;
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(smem + SL.lpt);       // [gbs*sp], phase E
+  int32_t* s_first = s_cnt + gbs * sp;
   for (int x = tid; x < gbs * sp; x += nt) {
-    const int q = x / sp, k = x % sp, F = p.fills[q];
+    const int q = x / sp, kk = x % sp, F = w.fills[q];
     const int base = F / sp, rem = F % sp;
-    p.shard_len[x] = base + (k < rem ? 1 : 0);
-    p.shard_start[x] = k * base + (k < rem ? k : rem);
-  }
-  __syncthreads();
-  for (int x = tid; x < W; x += nt) {  // x = r*sp + k
-    const int r = x / sp, k = x % sp;
-    int64_t acc = 0;
-    for (int j = 0; j < P; ++j) {
-      const int q = r * P + j;
-      p.row_base[q * sp + k] = acc;
-      acc += p.shard_len[q * sp + k];
-    }
-    p.llm_rows[x] = acc;
-  }
-  __syncthreads();
-
-  // ---- E. origin rank / origin_pos --------------------------------------------
-  int32_t* s_cnt = reinterpret_cast<int32_t*>(smem);        // [gbs*sp]
-  int32_t* s_first = s_cnt + gbs * sp;                       // [gbs*sp]
-  for (int x = tid; x < gbs * sp; x += nt) {
+    const int ln = base + (kk < rem ? 1 : 0);
+    const int st = kk * base + (kk < rem ? kk : rem);
+    p.shard_len[x] = ln;
+    p.shard_start[x] = st;
+    s_slen[x] = ln;
+    s_sstart[x] = st;
     s_cnt[x] = 0;
     s_first[x] = INT_MAX;
   }
   __syncthreads();
-  for (int i = tid; i < S; i += nt) {
-    const int q = p.seq[i];
-    p.group[i] = group_of_mod(mods[i]);
-    if (q < gbs) {
-      const int F = p.fills[q];
-      int pos = p.off[i];
-      if (pos > F - 1) pos = F - 1 > 0 ? F - 1 : 0;
-      int k = 0;
-      for (int kk = 0; kk < sp; ++kk)
-        if (p.shard_start[q * sp + kk] <= pos) k = kk;
-      p.origin[i] = (q / P) * sp + k;
-      p.scratch_a[i] = k;
-      if (p.group[i] < 0) {  // text: no encoder rows to move
-        p.arena_off[i] = -1;
-        p.enc_off[i] = -1;
-      }
-      atomicAdd(&s_cnt[q * sp + k], 1);
-      atomicMin(&s_first[q * sp + k], p.span[i]);
-    } else {
-      p.origin[i] = -1;
-      p.origin_pos[i] = -1;
-      p.enc[i] = -1;
-      p.arena_off[i] = -1;
-      p.enc_off[i] = -1;
-      p.llm_rank[i] = -1;
-      p.llm_row[i] = -1;
+  for (int x = tid; x < W; x += nt) {  // x = r*sp + k
+    const int r = x / sp, kk = x % sp;
+    int64_t acc = 0;
+    for (int j = 0; j < P; ++j) {
+      const int q = r * P + j;
+      p.row_base[q * sp + kk] = acc;
+      acc += s_slen[q * sp + kk];
     }
+    p.llm_rows[x] = acc;
+  }
+
+  // ---- E. origin rank (owner of the first token), origin_pos ----------------
+  stamp(p, 20);
+  for (int i = tid; i < S; i += nt) {
+    const int q = w.seq[i];
+    const int g = group_of_mod(mods[i]);
+    w.grp[i] = g;
+    if (q < gbs) {
+      const int F = w.fills[q];
+      int pos = w.off[i];
+      if (pos > F - 1) pos = F - 1 > 0 ? F - 1 : 0;
+      int kk = 0;
+      for (int j = 0; j < sp; ++j)
+        if (s_sstart[q * sp + j] <= pos) kk = j;
+      w.org[i] = (q / P) * sp + kk;
+      w.k[i] = kk;
+      atomicAdd(&s_cnt[q * sp + kk], 1);
+      atomicMin(&s_first[q * sp + kk], w.span[i]);
+    } else {
+      w.org[i] = -1;
+    }
+    w.opos[i] = -1;
+    w.enc[i] = -1;
+    w.aoff[i] = -1;
+    w.eoff[i] = -1;
   }
   __syncthreads();
   for (int x = tid; x < W; x += nt) {  // exclusive prefix of counts within (replica, shard)
-    const int r = x / sp, k = x % sp;
+    const int r = x / sp, kk = x % sp;
     int acc = 0;
     for (int j = 0; j < P; ++j) {
       const int q = r * P + j;
-      const int c = s_cnt[q * sp + k];
-      s_cnt[q * sp + k] = acc;
+      const int c = s_cnt[q * sp + kk];
+      s_cnt[q * sp + kk] = acc;
       acc += c;
     }
   }
   __syncthreads();
   int nbatch = 0;
   for (int i = tid; i < S; i += nt) {
-    const int q = p.seq[i];
+    const int q = w.seq[i];
     if (q < gbs) {
-      const int k = p.scratch_a[i];
-      p.origin_pos[i] = s_cnt[q * sp + k] + p.span[i] - s_first[q * sp + k];
+      const int kk = w.k[i];
+      w.opos[i] = s_cnt[q * sp + kk] + w.span[i] - s_first[q * sp + kk];
       ++nbatch;
     }
   }
@@ -672,230 +812,305 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(mux_plan_cfg cfg,
     block_excl_scan(nbatch, &tot, s_warp);
     if (tid == 0) p.hdr[MUX_H_N_BATCH] = tot;
   }
+  auto enc_item = [&](int i) { return w.seq[i] < gbs && w.grp[i] >= 0; };
 
-  // ---- F. loader arena offsets (origin, group) in table order ------------
-  auto enc_item = [&](int i) { return p.seq[i] < gbs && p.group[i] >= 0; };
-  keyed_scan(
-      S, W * MUX_N_GROUPS, [&](int i) { return enc_item(i) ? p.origin[i] * MUX_N_GROUPS + p.group[i] : -1; },
-      [&](int i) { return (int64_t)lens[i]; }, [&](int i, int64_t v) { p.arena_off[i] = v; },
-      s_tot, s_warp);
-  for (int x = tid; x < W * MUX_N_GROUPS; x += nt) p.arena_rows[x] = s_tot[x];
+  // ---- F. loader arena offsets: (origin, group) in table order ----------------
+  stamp(p, 21);
+  if (tid < kMaxKeys) s_carry[tid] = 0;
   __syncthreads();
-
-  // ---- G. encoder assignment per pool -------------------------------------------
-  LptSmem& ls = *reinterpret_cast<LptSmem*>(smem);
-  const int npools = cfg.pooled ? 1 : MUX_N_GROUPS;
-  for (int pool = 0; pool < npools; ++pool) {
-    auto in_pool = [&](int i) {
-      return enc_item(i) && (cfg.pooled || p.group[i] == pool);
-    };
-    // compact the pool in table order
-    keyed_scan(
-        S, 1, [&](int i) { return in_pool(i) ? 0 : -1; }, [&](int) { return (int64_t)1; },
-        [&](int i, int64_t v) {
-          ls.cost[v] = (double)lens[i];
-          ls.id[v] = ids[i];
-          ls.tidx[v] = i;
-        },
-        s_tot, s_warp);
-    const int m = (int)s_tot[0];
-    if (m == 0) continue;
-    if (W == 1) {
-      for (int k = tid; k < m; k += nt) ls.rank[k] = 0;
-    } else if (cfg.method == MUX_LPT) {
-      const int mpad = next_pow2(m);
-      for (int k = tid; k < mpad; k += nt) ls.ord[k] = k;
-      __syncthreads();
-      bitonic_sort(ls.ord, mpad, LptKey{ls.cost, ls.id, ls.tidx, m});
-      if (tid < 32) lpt_warp(ls.ord, ls.cost, m, W, ls.rank);
-    } else {
-      if (m > kKkMax) {
-        set_status(p, MUX_ERR_VALUE);
-        return;
-      }
-      // KK scratch lives after the LPT arrays (total < 227 KB)
-      KkSmem& K = *reinterpret_cast<KkSmem*>(smem + sizeof(LptSmem));
-      if (tid < 32) kk_warp(K, ls.cost, m, W, ls.rank);
-    }
-    __syncthreads();
-    for (int k = tid; k < m; k += nt) p.enc[ls.tidx[k]] = ls.rank[k];
-    __syncthreads();
+  for (int base = 0; base < S; base += nt) {
+    const int i = base + tid;
+    const bool e = i < S && enc_item(i);
+    const int key = e ? w.org[i] * MUX_N_GROUPS + w.grp[i] : -1;
+    const int64_t pre = multi_scan(key, e ? w.len[i] : 0, W * MUX_N_GROUPS, s_wk, s_carry);
+    if (e) w.aoff[i] = pre;
   }
-  for (int i = tid; i < S; i += nt)
-    if (p.seq[i] < gbs && p.group[i] < 0) p.enc[i] = -1;
+  for (int x = tid; x < W * MUX_N_GROUPS; x += nt) p.arena_rows[x] = s_carry[x];
+
+  // ---- G. encoder assignment: one sort over (pool, -cost, id, index), then
+  //         one warp per pool (LPT), or KK pool by pool --------------------------
+  stamp(p, 22);
+  const int npools = cfg.pooled ? 1 : MUX_N_GROUPS;
+  const int spad = next_pow2(S > 0 ? S : 1);
+  double* l_cost = reinterpret_cast<double*>(smem + SL.lpt);
+  int64_t* l_id = reinterpret_cast<int64_t*>(l_cost + spad);
+  int32_t* l_tidx = reinterpret_cast<int32_t*>(l_id + spad);
+  int32_t* l_pool = l_tidx + spad;
+  int32_t* l_ord = l_pool + spad;
+  int32_t* l_rank = l_ord + spad;
+  if (tid < kMaxKeys) s_carry[tid] = 0;
+  __syncthreads();
+  for (int base = 0; base < S; base += nt) {  // position of each encoder item in its pool
+    const int i = base + tid;
+    const bool e = i < S && enc_item(i);
+    const int pool = e ? (cfg.pooled ? 0 : w.grp[i]) : -1;
+    const int64_t pre = multi_scan(pool, 1, npools, s_wk, s_carry);
+    if (e) w.within[i] = (int32_t)pre;
+  }
+  if (tid == 0) {
+    s_misc[2] = (int)s_carry[0];
+    s_misc[3] = npools > 1 ? (int)s_carry[1] : 0;
+  }
+  __syncthreads();
+  const int m0 = s_misc[2], m1 = s_misc[3], m = m0 + m1;
+  for (int i = tid; i < S; i += nt) {  // pool-major item order
+    if (enc_item(i)) {
+      const int pool = cfg.pooled ? 0 : w.grp[i];
+      w.order[(pool == 0 ? 0 : m0) + w.within[i]] = i;
+    }
+  }
+  __syncthreads();
+  for (int v = tid; v < spad; v += nt) {
+    if (v < m) {
+      const int i = w.order[v];
+      l_cost[v] = (double)w.len[i];
+      l_id[v] = w.id[i];
+      l_tidx[v] = i;
+      l_pool[v] = v < m0 ? 0 : 1;
+    }
+    l_ord[v] = v;
+  }
+  __syncthreads();
+  if (m > 0) {
+    if (W == 1) {
+      for (int v = tid; v < m; v += nt) l_rank[v] = 0;
+    } else if (cfg.method == MUX_LPT) {
+      bitonic_sort(l_ord, next_pow2(m), PoolKey{l_pool, l_cost, l_id, l_tidx, m});
+      const int warp = tid >> 5;
+      if (warp == 0 && m0 > 0) lpt_warp(l_ord, l_cost, m0, W, l_rank);
+      if (warp == 1 && m1 > 0) lpt_warp(l_ord + m0, l_cost, m1, W, l_rank);
+    } else if (m0 > kKkMax || m1 > kKkMax) {
+      if (tid == 0) p.hdr[MUX_H_ERR_INDEX] = -2;  // KK pool limit
+    } else {
+      KkSmem& K = *reinterpret_cast<KkSmem*>(smem + SL.kk);
+      if (tid < 32 && m0 > 0) kk_warp(K, l_cost, m0, W, l_rank);
+      __syncthreads();
+      if (tid < 32 && m1 > 0) kk_warp(K, l_cost + m0, m1, W, l_rank + m0);
+    }
+  }
+  __syncthreads();
+  if (p.hdr[MUX_H_ERR_INDEX] == -2) {
+    emit(cfg, p, w, small, n_seq, false);
+    __syncthreads();
+    set_status(p, MUX_ERR_VALUE);
+    return;
+  }
+  for (int v = tid; v < m; v += nt) w.enc[l_tidx[v]] = l_rank[v];
   __syncthreads();
 
-  // ---- H. encoder order (origin, table index); encoder offsets -----------
-  keyed_scan(
-      S, W, [&](int i) { return enc_item(i) ? p.origin[i] : -1; }, [&](int) { return (int64_t)1; },
-      [&](int i, int64_t v) { p.scratch_b[i] = (int32_t)v; }, s_tot, s_warp);
+  // ---- H. encoder order = (origin rank, table index); encoder offsets ----------
+  stamp(p, 23);
+  if (tid < kMaxKeys) s_carry[tid] = 0;
+  __syncthreads();
+  for (int base = 0; base < S; base += nt) {  // index within origin rank
+    const int i = base + tid;
+    const bool e = i < S && enc_item(i);
+    const int64_t pre = multi_scan(e ? w.org[i] : -1, 1, W, s_wk, s_carry);
+    if (e) w.within[i] = (int32_t)pre;
+  }
   if (tid == 0) {
     int64_t acc = 0;
     for (int r = 0; r < W; ++r) {
-      const int64_t c = s_tot[r];
-      s_tot[32 + r] = acc;
+      const int64_t c = s_carry[r];
+      s_carry[r] = acc;
       acc += c;
     }
-    s_tot[32 + W] = acc;
+    s_misc[2] = (int)acc;
   }
   __syncthreads();
   for (int i = tid; i < S; i += nt)
-    if (enc_item(i)) p.order[s_tot[32 + p.origin[i]] + p.scratch_b[i]] = i;
+    if (enc_item(i)) w.order[s_carry[w.org[i]] + w.within[i]] = i;
   __syncthreads();
-  const int n_enc = (int)s_tot[32 + W];
-  keyed_scan(
-      n_enc, W * MUX_N_GROUPS,
-      [&](int t) { const int i = p.order[t]; return p.enc[i] * MUX_N_GROUPS + p.group[i]; },
-      [&](int t) { return (int64_t)lens[p.order[t]]; },
-      [&](int t, int64_t v) { p.enc_off[p.order[t]] = v; }, s_tot, s_warp);
-  for (int x = tid; x < W * MUX_N_GROUPS; x += nt) p.recv_rows[x] = s_tot[x];
+  const int n_enc = s_misc[2];
+  if (tid < kMaxKeys) s_carry[tid] = 0;
+  __syncthreads();
+  for (int base = 0; base < n_enc; base += nt) {
+    const int t = base + tid;
+    const int i = t < n_enc ? w.order[t] : 0;
+    const int key = t < n_enc ? w.enc[i] * MUX_N_GROUPS + w.grp[i] : -1;
+    const int64_t pre =
+        multi_scan(key, t < n_enc ? w.len[i] : 0, W * MUX_N_GROUPS, s_wk, s_carry);
+    if (t < n_enc) w.eoff[i] = pre;
+  }
+  for (int x = tid; x < W * MUX_N_GROUPS; x += nt) p.recv_rows[x] = s_carry[x];
   __syncthreads();
 
-  // ---- I. LLM positions, return pieces and segment tables of rank `me` ----
+  // ---- I. LLM positions, return pieces and segment tables of rank `me` -------
+  stamp(p, 24);
   const int me = cfg.me;
   auto owner_k = [&](int q, int pos) {
-    int k = 0;
-    for (int kk = 0; kk < sp; ++kk)
-      if (p.shard_start[q * sp + kk] <= pos) k = kk;
-    return k;
+    int kk = 0;
+    for (int j = 0; j < sp; ++j)
+      if (s_sstart[q * sp + j] <= pos) kk = j;
+    return kk;
   };
-  auto npieces = [&](int i) {
-    const int L = lens[i];
-    if (L <= 0) return 0;
-    const int q = p.seq[i];
-    return owner_k(q, p.off[i] + L - 1) - owner_k(q, p.off[i]) + 1;
-  };
-  for (int i = tid; i < S; i += nt) {
-    if (enc_item(i)) {
-      const int q = p.seq[i];
-      const int pos = p.off[i];
-      const int k = owner_k(q, pos < p.fills[q] ? pos : (p.fills[q] > 0 ? p.fills[q] - 1 : 0));
-      p.llm_rank[i] = (q / P) * sp + k;
-      p.llm_row[i] = p.row_base[q * sp + k] + pos - p.shard_start[q * sp + k];
-    } else if (p.seq[i] < gbs) {
+  const int64_t CH = cfg.chunk_bytes > 0 ? cfg.chunk_bytes : kDefaultChunkBytes;
+  int64_t dcarry = 0, rcarry = 0, dchunks = 0, rchunks = 0;
+  int64_t dbytes = 0, rbytes = 0, dremote = 0, rremote = 0;
+  for (int base = 0; base < S; base += nt) {
+    const int i = base + tid;
+    const bool e = i < S && enc_item(i);
+    int npieces = 0, q = 0, L = 0, off = 0, g = 0;
+    if (e) {
+      q = w.seq[i];
+      L = w.len[i];
+      off = w.off[i];
+      g = w.grp[i];
+      const int F = w.fills[q];
+      const int k0 = owner_k(q, off < F ? off : (F > 0 ? F - 1 : 0));
+      p.llm_rank[i] = (q / P) * sp + k0;
+      p.llm_row[i] = p.row_base[q * sp + k0] + off - s_sstart[q * sp + k0];
+      if (w.enc[i] == me && L > 0) npieces = owner_k(q, off + L - 1) - owner_k(q, off) + 1;
+    } else if (i < S) {
       p.llm_rank[i] = -1;
       p.llm_row[i] = -1;
     }
-  }
-  // dispatch segments: samples of `me` with rows to move, table order
-  keyed_scan(
-      S, 1, [&](int i) { return enc_item(i) && p.origin[i] == me && lens[i] > 0 ? 0 : -1; },
-      [&](int) { return (int64_t)1; },
-      [&](int i, int64_t v) {
-        p.dsrc[v] = p.arena_off[i];
-        p.ddst[v] = p.enc_off[i];
-        p.drows[v] = lens[i];
-        p.dgroup[v] = p.group[i];
-        p.drank[v] = p.enc[i];
-      },
-      s_tot, s_warp);
-  const int nd = (int)s_tot[0];
-  // return pieces: samples encoded on `me`, split at Ulysses shard borders
-  keyed_scan(
-      S, 1, [&](int i) { return enc_item(i) && p.enc[i] == me ? 0 : -1; },
-      [&](int i) { return (int64_t)npieces(i); },
-      [&](int i, int64_t v) {
-        const int q = p.seq[i], L = lens[i];
-        int t = 0, slot = (int)v;
-        while (t < L) {
-          const int pos = p.off[i] + t;
-          const int k = owner_k(q, pos);
-          const int end = p.shard_start[q * sp + k] + p.shard_len[q * sp + k];
-          const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
-          p.rsrc[slot] = p.enc_off[i] + t;
-          p.rdst[slot] = p.row_base[q * sp + k] + pos - p.shard_start[q * sp + k];
-          p.rrows[slot] = n;
-          p.rgroup[slot] = p.group[i];
-          p.rrank[slot] = (q / P) * sp + k;
-          ++slot;
-          t += n;
-        }
-      },
-      s_tot, s_warp);
-  const int nr = (int)s_tot[0];
-
-  // chunk prefix + chunk maps for both tables
-  const int64_t CH = cfg.chunk_bytes > 0 ? cfg.chunk_bytes : kDefaultChunkBytes;
-  for (int which = 0; which < 2; ++which) {
-    const int n = which == 0 ? nd : nr;
-    int64_t* rows = which == 0 ? p.drows : p.rrows;
-    int32_t* grp = which == 0 ? p.dgroup : p.rgroup;
-    int32_t* rk = which == 0 ? p.drank : p.rrank;
-    int64_t* c0 = which == 0 ? p.dchunk0 : p.rchunk0;
-    int32_t* cmap = which == 0 ? p.dchunk_seg : p.rchunk_seg;
-    const int32_t* rb = which == 0 ? cfg.row_bytes_in : cfg.row_bytes_ret;
-    int64_t carry = 0, bytes = 0, remote = 0;
-    for (int base = 0; base < n; base += nt) {
-      const int s = base + tid;
-      int64_t nbytes = 0, nchk = 0;
-      if (s < n) {
-        nbytes = rows[s] * (int64_t)rb[grp[s]];
-        nchk = (nbytes + CH - 1) / CH;
-      }
-      int64_t tot;
-      const int64_t pre = block_excl_scan(nchk, &tot, s_warp);
-      if (s < n) c0[s] = carry + pre;
-      carry += tot;
-      int64_t tb, trm;
-      block_excl_scan(nbytes, &tb, s_warp);
-      block_excl_scan(s < n && rk[s] != me ? nbytes : 0, &trm, s_warp);
-      bytes += tb;
-      remote += trm;
+    const bool disp = e && w.org[i] == me && L > 0;
+    int64_t tot, tchk;
+    // dispatch segment (one per sample of `me`)
+    const int64_t dslot = block_excl_scan(disp ? 1 : 0, &tot, s_warp);
+    const int64_t dbytes_i = disp ? (int64_t)L * cfg.row_bytes_in[g] : 0;
+    const int64_t dchk_pre = block_excl_scan((dbytes_i + CH - 1) / CH, &tchk, s_warp);
+    if (disp) {
+      const int64_t v = dcarry + dslot;
+      p.dsrc[v] = w.aoff[i];
+      p.ddst[v] = w.eoff[i];
+      p.drows[v] = L;
+      p.dgroup[v] = g;
+      p.drank[v] = w.enc[i];
+      p.dchunk0[v] = dchunks + dchk_pre;
+      dbytes += dbytes_i;
+      if (w.enc[i] != me) dremote += dbytes_i;
     }
+    dcarry += tot;
+    dchunks += tchk;
+    // return pieces (one per Ulysses shard the sample touches)
+    const int64_t rslot = block_excl_scan(npieces, &tot, s_warp);
+    int64_t rchk = 0;
+    for (int t = 0; npieces && t < L;) {
+      const int pos = off + t, kk = owner_k(q, pos);
+      const int end = s_sstart[q * sp + kk] + s_slen[q * sp + kk];
+      const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
+      rchk += ((int64_t)n * cfg.row_bytes_ret[g] + CH - 1) / CH;
+      t += n;
+    }
+    const int64_t rchk_pre = block_excl_scan(rchk, &tchk, s_warp);
+    int slot = (int)(rcarry + rslot);
+    int64_t c0 = rchunks + rchk_pre;
+    for (int t = 0; npieces && t < L;) {
+      const int pos = off + t, kk = owner_k(q, pos);
+      const int end = s_sstart[q * sp + kk] + s_slen[q * sp + kk];
+      const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
+      const int dst = (q / P) * sp + kk;
+      const int64_t nb = (int64_t)n * cfg.row_bytes_ret[g];
+      p.rsrc[slot] = w.eoff[i] + t;
+      p.rdst[slot] = p.row_base[q * sp + kk] + pos - s_sstart[q * sp + kk];
+      p.rrows[slot] = n;
+      p.rgroup[slot] = g;
+      p.rrank[slot] = dst;
+      p.rchunk0[slot] = c0;
+      c0 += (nb + CH - 1) / CH;
+      rbytes += nb;
+      if (dst != me) rremote += nb;
+      ++slot;
+      t += n;
+    }
+    rcarry += tot;
+    rchunks += tchk;
+  }
+  {
+    int64_t t0, t1, t2, t3;
+    block_excl_scan(dbytes, &t0, s_warp);
+    block_excl_scan(rbytes, &t1, s_warp);
+    block_excl_scan(dremote, &t2, s_warp);
+    block_excl_scan(rremote, &t3, s_warp);
     if (tid == 0) {
-      c0[n] = carry;
-      p.hdr[which == 0 ? MUX_H_DISPATCH_CHUNKS : MUX_H_RETURN_CHUNKS] = carry;
-      p.hdr[which == 0 ? MUX_H_DISPATCH_BYTES : MUX_H_RETURN_BYTES] = bytes;
-      p.hdr[which == 0 ? MUX_H_DISPATCH_REMOTE : MUX_H_RETURN_REMOTE] = remote;
+      p.dchunk0[dcarry] = dchunks;
+      p.rchunk0[rcarry] = rchunks;
+      p.hdr[MUX_H_DISPATCH_CHUNKS] = dchunks;
+      p.hdr[MUX_H_RETURN_CHUNKS] = rchunks;
+      p.hdr[MUX_H_DISPATCH_BYTES] = t0;
+      p.hdr[MUX_H_RETURN_BYTES] = t1;
+      p.hdr[MUX_H_DISPATCH_REMOTE] = t2;
+      p.hdr[MUX_H_RETURN_REMOTE] = t3;
+      p.hdr[MUX_H_N_DISPATCH] = dcarry;
+      p.hdr[MUX_H_N_RETURN] = rcarry;
+      p.hdr[MUX_H_RECV_ROWS0] = p.recv_rows[me * MUX_N_GROUPS + 0];
+      p.hdr[MUX_H_RECV_ROWS1] = p.recv_rows[me * MUX_N_GROUPS + 1];
     }
-    __syncthreads();
-    if (carry > cfg.max_chunks) {
-      set_status(p, MUX_ERR_RUNTIME);
-      return;
-    }
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int s = warp; s < n; s += nt / 32)
-      for (int64_t c = c0[s] + lane; c < c0[s + 1]; c += 32) cmap[c] = s;
   }
-  if (tid == 0) {
-    p.hdr[MUX_H_N_DISPATCH] = nd;
-    p.hdr[MUX_H_N_RETURN] = nr;
-    p.hdr[MUX_H_RECV_ROWS0] = p.recv_rows[me * MUX_N_GROUPS + 0];
-    p.hdr[MUX_H_RECV_ROWS1] = p.recv_rows[me * MUX_N_GROUPS + 1];
-    p.hdr[MUX_H_STATUS] = MUX_OK;
+  emit(cfg, p, w, small, n_seq, true);
+  stamp(p, 25);
+  __syncthreads();
+  set_status(p, MUX_OK);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    plan_kernel(mux_plan_cfg cfg, const int32_t* lens, const int32_t* mods, const int64_t* ids,
+                const int32_t* carry_seq, const int32_t* chunk_off, Plan p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t s_warp[33];
+  __shared__ bool s_last;
+  if (blockIdx.x == 0) stamp(p, 16);
+  if (cfg.n_chunks > 0) ffd_chunk(cfg, lens, ids, chunk_off, p, smem, s_warp);
+  // the last CTA to arrive finalises the step
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t t = atomicAdd(p.ticket, 1u);
+    s_last = t == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x == 0) *p.ticket = 0;  // re-arm for the next plan
+  __threadfence();
+  finalize(cfg, lens, mods, ids, carry_seq, chunk_off, p, smem, s_warp);
 }
 
 // Stand-alone partition (kk_partition / LPT) of one pool.
-__global__ void __launch_bounds__(kFinThreads) assign_kernel(int method, const double* w,
+__global__ void __launch_bounds__(kThreads, 1) assign_kernel(int method, const double* w,
                                                              const int64_t* ids, int n, int g,
                                                              int32_t* out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  LptSmem& ls = *reinterpret_cast<LptSmem*>(smem);
-  for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    ls.cost[k] = w[k];
-    ls.id[k] = ids ? ids[k] : k;
-    ls.tidx[k] = k;
+  const int npad = next_pow2(n > 0 ? n : 1);
+  double* cost = reinterpret_cast<double*>(smem);
+  int64_t* id = reinterpret_cast<int64_t*>(cost + npad);
+  int32_t* tidx = reinterpret_cast<int32_t*>(id + npad);
+  int32_t* pool = tidx + npad;
+  int32_t* ord = pool + npad;
+  int32_t* rank = ord + npad;
+  for (int k = threadIdx.x; k < npad; k += blockDim.x) {
+    if (k < n) {
+      cost[k] = w[k];
+      id[k] = ids ? ids[k] : k;
+      tidx[k] = k;
+      pool[k] = 0;
+    }
+    ord[k] = k;
   }
   __syncthreads();
   if (g == 1) {
-    for (int k = threadIdx.x; k < n; k += blockDim.x) ls.rank[k] = 0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) rank[k] = 0;
   } else if (method == MUX_LPT) {
-    const int npad = next_pow2(n > 0 ? n : 1);
-    for (int k = threadIdx.x; k < npad; k += blockDim.x) ls.ord[k] = k;
-    __syncthreads();
-    bitonic_sort(ls.ord, npad, LptKey{ls.cost, ls.id, ls.tidx, n});
-    if (threadIdx.x < 32) lpt_warp(ls.ord, ls.cost, n, g, ls.rank);
+    bitonic_sort(ord, npad, PoolKey{pool, cost, id, tidx, n});
+    if (threadIdx.x < 32) lpt_warp(ord, cost, n, g, rank);
   } else {
-    KkSmem& K = *reinterpret_cast<KkSmem*>(smem + sizeof(LptSmem));
-    if (threadIdx.x < 32) kk_warp(K, ls.cost, n, g, ls.rank);
+    KkSmem& K = *reinterpret_cast<KkSmem*>(smem + align_up(32 * npad, 16));
+    if (threadIdx.x < 32) kk_warp(K, cost, n, g, rank);
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < n; k += blockDim.x) out[k] = ls.rank[k];
+  for (int k = threadIdx.x; k < n; k += blockDim.x) out[k] = rank[k];
 }
 
-static size_t finalize_smem() {
-  return sizeof(LptSmem) + sizeof(KkSmem);  // 206,848 B < 227 KB
+static int plan_smem_bytes(const mux_plan_cfg& c) {
+  const int max_seq = c.n_carry_seqs + (c.S - c.n_carry) + 1;
+  const int gb = c.mode == MUX_MODE_STEP ? c.gbs * c.sp : 0;
+  const SmemPlan SL = smem_plan(c.S, max_seq, gb, c.method);
+  int maxn = c.S - c.n_carry;
+  int npad = 1;
+  while (npad < maxn) npad <<= 1;
+  const int ffd = 24 * npad;
+  return SL.total > ffd ? SL.total : ffd;
 }
 
 }  // namespace mux
@@ -910,6 +1125,8 @@ extern "C" int mux_plan_layout_of(const mux_plan_cfg* cfg, mux_plan_layout* out)
   return compute_layout(*cfg, out);
 }
 
+static constexpr int kSmemLimit = 227 * 1024 - 10 * 1024;  // leave room for static shared
+
 extern "C" int mux_plan_step(const mux_plan_cfg* cfg, const int32_t* lens, const int32_t* mods,
                              const int64_t* ids, const int32_t* carry_seq,
                              const int32_t* chunk_off, void* plan, size_t plan_bytes,
@@ -921,38 +1138,28 @@ extern "C" int mux_plan_step(const mux_plan_cfg* cfg, const int32_t* lens, const
     set_error("plan buffer of %zu bytes, need %lld", plan_bytes, (long long)L.total);
     return MUX_ERR_VALUE;
   }
-  if (cfg->n_chunks > 1024) {
-    set_error("more than 1024 chunks in one step");
-    return MUX_ERR_VALUE;
-  }
   if (cfg->mode == MUX_MODE_STEP && (cfg->me < 0 || cfg->me >= cfg->world)) {
     set_error("rank %d outside world %d", cfg->me, cfg->world);
     return MUX_ERR_VALUE;
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  Plan p = make_plan(plan, L);
-  MUX_CUDA(cudaMemsetAsync(p.hdr, 0xff, 8 * MUX_H_SLOTS, s));
+  const int smem = plan_smem_bytes(*cfg);
+  if (smem > kSmemLimit) {
+    set_error("plan of %d samples needs %d B of shared memory (limit %d)", cfg->S, smem,
+              kSmemLimit);
+    return MUX_ERR_VALUE;
+  }
   static bool attr_done = false;
   if (!attr_done) {
-    MUX_CUDA(cudaFuncSetAttribute(ffd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  4096 * 24));
-    MUX_CUDA(cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)finalize_smem()));
+    MUX_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimit));
     MUX_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)finalize_smem()));
+                                  kSmemLimit));
     attr_done = true;
   }
-  if (cfg->n_chunks > 0) {
-    // worst chunk size bounds the shared memory: npad * (8 + 4*4)
-    int maxn = cfg->S - cfg->n_carry;
-    int npad = 1;
-    while (npad < maxn) npad <<= 1;
-    ffd_kernel<<<cfg->n_chunks, kFfdThreads, (size_t)npad * 24, s>>>(*cfg, lens, ids, chunk_off,
-                                                                      p);
-    MUX_CUDA(cudaGetLastError());
-  }
-  finalize_kernel<<<1, kFinThreads, finalize_smem(), s>>>(*cfg, lens, mods, ids, carry_seq,
-                                                           chunk_off, p);
+  Plan p = make_plan(plan, L);
+  const int grid = cfg->n_chunks > 0 ? cfg->n_chunks : 1;
+  plan_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      *cfg, lens, mods, ids, carry_seq, chunk_off, p);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }
@@ -976,15 +1183,11 @@ extern "C" int mux_plan_check(const mux_plan_cfg* cfg, const int64_t* h, const i
                   cfg->dp, cfg->mbs);
       return MUX_ERR_CONFIG;
     case MUX_ERR_VALUE:
-      if (h[MUX_H_N_SEQ] < cfg->gbs) {
-        set_error("need %d sequences, have %lld", cfg->gbs, (long long)h[MUX_H_N_SEQ]);
-      } else {
+      if (h[MUX_H_ERR_INDEX] == -2)
         set_error("encoder pool larger than the KK limit %d", kKkMax);
-      }
+      else
+        set_error("need %d sequences, have %lld", cfg->gbs, (long long)h[MUX_H_N_SEQ]);
       return MUX_ERR_VALUE;
-    case MUX_ERR_RUNTIME:
-      set_error("copy chunk map overflow (max_chunks %d)", cfg->max_chunks);
-      return MUX_ERR_RUNTIME;
     default:
       set_error("plan did not complete (status %lld)", (long long)st);
       return MUX_ERR_RUNTIME;
@@ -1004,10 +1207,13 @@ extern "C" int mux_assign(int32_t method, const double* w, const int64_t* ids, i
     return MUX_ERR_VALUE;
   }
   if (n == 0) return MUX_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int npad = 1;
+  while (npad < n) npad <<= 1;
+  const int smem = (int)align_up(32 * npad, 16) + (method == MUX_KK ? (int)sizeof(KkSmem) : 0);
   MUX_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)finalize_smem()));
-  assign_kernel<<<1, kFinThreads, finalize_smem(), s>>>(method, w, ids, n, g, out);
+                                kSmemLimit));
+  assign_kernel<<<1, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(method, w, ids, n, g,
+                                                                          out);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

@@ -76,7 +76,7 @@ __device__ __forceinline__ void copy_block(char* dst, const char* src, int64_t n
 
 struct SegArgs {
   const int64_t* hdr_chunks;  // total chunks
-  const int32_t* cmap;
+  const int64_t* hdr_segs;    // number of segments
   const int64_t *chunk0, *src_row, *dst_row, *rows;
   const int32_t *group, *rank;
   int64_t chunk_bytes;
@@ -91,19 +91,42 @@ struct SegArgs {
   int32_t me, world;
 };
 
-__global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a) {
+// Each CTA copies a contiguous range of chunks, so it locates its first
+// segment once (binary search over the chunk prefix, staged in shared memory
+// when it fits) and then walks forward.
+__global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int smem_segs) {
+  extern __shared__ int32_t s_c0[];
   const int64_t nchunks = *a.hdr_chunks;
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const int s = a.cmap[c];
-    const int g = a.group[s];
-    const int64_t rb = a.row_bytes[g];
-    const int64_t lo = (c - a.chunk0[s]) * a.chunk_bytes;
-    const int64_t seg = a.rows[s] * rb;
-    const int64_t n = seg - lo < a.chunk_bytes ? seg - lo : a.chunk_bytes;
-    const char* src = static_cast<const char*>(a.src_bases[g]) + a.src_row[s] * rb + lo;
-    const int di = a.per_group_dst ? a.rank[s] * MUX_N_GROUPS + g : a.rank[s];
-    char* dst = static_cast<char*>(a.dst_bases[di]) + a.dst_row[s] * rb + lo;
-    copy_block(dst, src, n);
+  const int nseg = (int)*a.hdr_segs;
+  const bool staged = nseg < smem_segs;
+  if (staged) {
+    for (int i = threadIdx.x; i <= nseg; i += blockDim.x) s_c0[i] = (int32_t)a.chunk0[i];
+    __syncthreads();
+  }
+  auto c0 = [&](int s) -> int64_t { return staged ? s_c0[s] : a.chunk0[s]; };
+  const int64_t c_begin = nchunks * blockIdx.x / gridDim.x;
+  const int64_t c_end = nchunks * (blockIdx.x + 1) / gridDim.x;
+  if (c_begin < c_end) {
+    int lo = 0, hi = nseg - 1;  // last segment with c0 <= c_begin
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (c0(mid) <= c_begin) lo = mid;
+      else hi = mid - 1;
+    }
+    int s = lo;
+    int64_t next = c0(s + 1);
+    for (int64_t c = c_begin; c < c_end; ++c) {
+      while (c >= next) next = c0(++s + 1);
+      const int g = a.group[s];
+      const int64_t rb = a.row_bytes[g];
+      const int64_t lo_b = (c - c0(s)) * a.chunk_bytes;
+      const int64_t seg = a.rows[s] * rb;
+      const int64_t n = seg - lo_b < a.chunk_bytes ? seg - lo_b : a.chunk_bytes;
+      const char* src = static_cast<const char*>(a.src_bases[g]) + a.src_row[s] * rb + lo_b;
+      const int di = a.per_group_dst ? a.rank[s] * MUX_N_GROUPS + g : a.rank[s];
+      char* dst = static_cast<char*>(a.dst_bases[di]) + a.dst_row[s] * rb + lo_b;
+      copy_block(dst, src, n);
+    }
   }
   if (a.flags_peers) {
     __threadfence_system();  // every thread's peer stores before the CTA's arrival
@@ -254,7 +277,7 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
   SegArgs a;
   const bool ret = which != 0;
   a.hdr_chunks = p.hdr + (ret ? MUX_H_RETURN_CHUNKS : MUX_H_DISPATCH_CHUNKS);
-  a.cmap = ret ? p.rchunk_seg : p.dchunk_seg;
+  a.hdr_segs = p.hdr + (ret ? MUX_H_N_RETURN : MUX_H_N_DISPATCH);
   a.chunk0 = ret ? p.rchunk0 : p.dchunk0;
   a.src_row = ret ? p.rsrc : p.dsrc;
   a.dst_row = ret ? p.rdst : p.ddst;
@@ -277,7 +300,11 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
     return MUX_ERR_VALUE;
   }
   const int grid = grid_ctas > 0 ? grid_ctas : num_sms() * 8;
-  segcopy_kernel<<<grid, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  // stage the chunk prefix in shared memory when the segment bound is small
+  const int max_segs = ret ? cfg->S * (cfg->sp + 1) + 1 : cfg->S + 1;
+  const int smem_segs = max_segs + 1 <= 4096 ? max_segs + 1 : 0;
+  segcopy_kernel<<<grid, kCopyThreads, smem_segs * sizeof(int32_t),
+                   static_cast<cudaStream_t>(stream)>>>(a, smem_segs);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

@@ -113,12 +113,6 @@ class DeviceTable:
         self.chunk_off = i32 + 4 * (2 * S + nc)
 
 
-def chunk_bound(capacity: int, gbs: int, sp: int, S: int, row_bytes, chunk_bytes: int) -> int:
-    """Upper bound on copy chunks of one table (all batch tokens, widest row)."""
-    tok = max(gbs, 1) * capacity
-    return (tok * max(row_bytes) + chunk_bytes - 1) // chunk_bytes + S * (sp + 1) + 1
-
-
 def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int = 1,
              world: int = 1, mbs: int = 1, method: str = "lpt", pooled: bool = False,
              me: int = 0, mode: int = _lib.MODE_STEP, row_bytes_in=(1176, 1024),
@@ -134,8 +128,6 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
         c.row_bytes_in[g] = row_bytes_in[g]
         c.row_bytes_ret[g] = row_bytes_ret[g]
     c.chunk_bytes = chunk_bytes
-    c.max_chunks = max(chunk_bound(capacity, gbs, sp, table.S, row_bytes_in, chunk_bytes),
-                       chunk_bound(capacity, gbs, sp, table.S, row_bytes_ret, chunk_bytes))
     return c
 
 
@@ -159,7 +151,8 @@ class Plan:
         self.cfg = cfg
         self.layout = layout_of(cfg)
         if blob is None or blob.numel() < self.layout.total:
-            blob = torch.empty(self.layout.total, dtype=torch.uint8, device=device)
+            # zero-filled: the kernel's last-CTA ticket must start at 0
+            blob = torch.zeros(self.layout.total, dtype=torch.uint8, device=device)
         self.blob = blob
 
     @property
