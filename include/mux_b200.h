@@ -144,21 +144,21 @@ int mux_assign(int32_t method, const double* weights, const int64_t* ids, int32_
 /* Segment copy: table = plan (dispatch: which=0, return: which=1).
  * src_bases[group], dst_bases[rank * MUX_N_GROUPS + group] (dispatch) or
  * dst_bases[rank] (return) are device arrays of device pointers (local or
- * NVLink-peer).  row bytes come from the plan cfg.  grid_ctas = 0 picks
- * the persistent default (148 SMs x occupancy). */
+ * NVLink-peer).  Row bytes come from the plan cfg.  CTAs grab chunks from a
+ * device counter: `sync` is uint32[2] in device memory, zero before the first
+ * launch and re-armed by the kernel.  grid_ctas = 0 picks the persistent
+ * default (SMs x occupancy). */
 int mux_segcopy(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                 void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
-                void* stream);
+                uint32_t* sync, void* stream);
 /* Same copy, then the last CTA advances the device epoch counter
  * (e = ++*epoch_ctr), fences at system scope and stores e into
- * flags_peers[r][me] for every rank r (fused completion signal).
- * done_counter: one zero-initialised uint32 in device memory, re-armed by
- * the kernel itself.  Epochs live in device memory, so a captured CUDA graph
- * of the step replays correctly. */
+ * flags_peers[r][me] for every rank r (fused completion signal).  Epochs live
+ * in device memory, so a captured CUDA graph of the step replays correctly. */
 int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                        void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
-                       uint64_t* const* flags_peers, uint32_t* done_counter,
-                       uint64_t* epoch_ctr, void* stream);
+                       uint64_t* const* flags_peers, uint32_t* sync, uint64_t* epoch_ctr,
+                       void* stream);
 
 /* Cross-GPU completion flags.  flags_peers: device array of `world` device
  * pointers to each rank's uint64 flag array (world entries each).  signal

@@ -54,7 +54,7 @@ _SIGS = [
     ("mux_plan_check", C.c_int, [C.POINTER(PlanCfg), _P, _P, _P]),
     ("mux_assign_scratch_bytes", C.c_size_t, [C.c_int32, C.c_int32]),
     ("mux_assign", C.c_int, [C.c_int32, _P, _P, C.c_int32, C.c_int32, _P, _P, _P]),
-    ("mux_segcopy", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, _P, C.c_int32, _P]),
+    ("mux_segcopy", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, _P, C.c_int32, _P, _P]),
     ("mux_segcopy_signal", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, _P, C.c_int32, _P,
                                      _P, _P, _P]),
     ("mux_signal", C.c_int, [C.c_int32, C.c_int32, _P, _P, _P]),

@@ -1158,7 +1158,12 @@ extern "C" int mux_plan_step(const mux_plan_cfg* cfg, const int32_t* lens, const
   }
   Plan p = make_plan(plan, L);
   const int grid = cfg->n_chunks > 0 ? cfg->n_chunks : 1;
-  plan_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+  // Block size follows the step: every phase is a handful of barriers and
+  // block scans whose cost grows with the warp count, so small steps (S of a
+  // few hundred) run with 4-8 warps.
+  int threads = ((cfg->S + 31) / 32) * 32;
+  threads = threads < 128 ? 128 : (threads > kThreads ? kThreads : threads);
+  plan_kernel<<<grid, threads, smem, static_cast<cudaStream_t>(stream)>>>(
       *cfg, lens, mods, ids, carry_seq, chunk_off, p);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;

@@ -85,28 +85,36 @@ struct SegArgs {
   void* const* src_bases;
   void* const* dst_bases;
   // fused completion signal (optional)
+  uint32_t* sync;       // [0] chunk counter, [1] CTAs done (zero between launches)
   uint64_t* const* flags_peers;
-  uint32_t* done_counter;
   uint64_t* epoch_ctr;  // device counter: epoch = ++*epoch_ctr (graph-replay safe)
   int32_t me, world;
 };
 
-// Each CTA copies a contiguous range of chunks, so it locates its first
-// segment once (binary search over the chunk prefix, staged in shared memory
-// when it fits) and then walks forward.
+// Work distribution is dynamic: CTAs grab kGrab chunks at a time from a
+// device counter (the next grab is fetched while the current one copies), so
+// CTAs that start late — e.g. next to the side-stream planner — take less.
+// Each grab locates its first segment by binary search over the chunk prefix
+// (staged in shared memory when it fits) and walks forward.
+constexpr int kGrab = 4;
+
 __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int smem_segs) {
   extern __shared__ int32_t s_c0[];
+  __shared__ uint32_t s_grab[2];
+  __shared__ bool s_last;
   const int64_t nchunks = *a.hdr_chunks;
   const int nseg = (int)*a.hdr_segs;
   const bool staged = nseg < smem_segs;
-  if (staged) {
+  if (staged)
     for (int i = threadIdx.x; i <= nseg; i += blockDim.x) s_c0[i] = (int32_t)a.chunk0[i];
-    __syncthreads();
-  }
+  if (threadIdx.x == 0) s_grab[0] = atomicAdd(&a.sync[0], (uint32_t)kGrab);
+  __syncthreads();
   auto c0 = [&](int s) -> int64_t { return staged ? s_c0[s] : a.chunk0[s]; };
-  const int64_t c_begin = nchunks * blockIdx.x / gridDim.x;
-  const int64_t c_end = nchunks * (blockIdx.x + 1) / gridDim.x;
-  if (c_begin < c_end) {
+  for (int buf = 0;; buf ^= 1) {
+    const int64_t c_begin = s_grab[buf];
+    if (c_begin >= nchunks) break;
+    if (threadIdx.x == 0) s_grab[buf ^ 1] = atomicAdd(&a.sync[0], (uint32_t)kGrab);
+    const int64_t c_end = c_begin + kGrab < nchunks ? c_begin + kGrab : nchunks;
     int lo = 0, hi = nseg - 1;  // last segment with c0 <= c_begin
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -127,28 +135,27 @@ __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int sm
       char* dst = static_cast<char*>(a.dst_bases[di]) + a.dst_row[s] * rb + lo_b;
       copy_block(dst, src, n);
     }
+    __syncthreads();
+  }
+  // completion: the last CTA re-arms the counters and, for an exchange, fences
+  // at system scope and publishes the next epoch to every peer
+  if (a.flags_peers) __threadfence_system();  // this thread's peer stores first
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.sync[1], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last || threadIdx.x >= 32) return;
+  if (threadIdx.x == 0) {
+    a.sync[0] = 0;
+    a.sync[1] = 0;
   }
   if (a.flags_peers) {
-    __threadfence_system();  // every thread's peer stores before the CTA's arrival
-    __syncthreads();
-    __shared__ bool last;
-    if (threadIdx.x == 0) {
-      const uint32_t t = atomicAdd(a.done_counter, 1u);
-      last = t == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (last && threadIdx.x < 32) {
-      const uint64_t e = *a.epoch_ctr + 1;
-      __syncwarp();
-      if (threadIdx.x == 0) {
-        *a.epoch_ctr = e;
-        *a.done_counter = 0;  // re-arm for the next launch
-      }
-      __threadfence_system();
-      if (threadIdx.x < a.world) {
-        uint64_t* f = a.flags_peers[threadIdx.x] + a.me;
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
-      }
+    const uint64_t e = *a.epoch_ctr + 1;
+    __syncwarp();
+    if (threadIdx.x == 0) *a.epoch_ctr = e;
+    __threadfence_system();
+    if (threadIdx.x < a.world) {
+      uint64_t* f = a.flags_peers[threadIdx.x] + a.me;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
     }
   }
 }
@@ -261,15 +268,15 @@ using namespace mux;
 
 extern "C" int mux_segcopy(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                            void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
-                           void* stream) {
-  return mux_segcopy_signal(cfg, plan, which, src_bases, dst_bases, grid_ctas, nullptr, nullptr,
+                           uint32_t* sync, void* stream) {
+  return mux_segcopy_signal(cfg, plan, which, src_bases, dst_bases, grid_ctas, nullptr, sync,
                             nullptr, stream);
 }
 
 extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                                   void* const* src_bases, void* const* dst_bases,
                                   int32_t grid_ctas, uint64_t* const* flags_peers,
-                                  uint32_t* done_counter, uint64_t* epoch_ctr, void* stream) {
+                                  uint32_t* sync, uint64_t* epoch_ctr, void* stream) {
   mux_plan_layout L;
   int st = mux_plan_layout_of(cfg, &L);
   if (st) return st;
@@ -291,12 +298,12 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
   a.src_bases = src_bases;
   a.dst_bases = dst_bases;
   a.flags_peers = flags_peers;
-  a.done_counter = done_counter;
+  a.sync = sync;
   a.epoch_ctr = epoch_ctr;
   a.me = cfg->me;
   a.world = cfg->world;
-  if (flags_peers && (!done_counter || !epoch_ctr)) {
-    set_error("signal requested without completion/epoch counters");
+  if (!sync || (flags_peers && !epoch_ctr)) {
+    set_error("segment copy needs its sync counters (and an epoch counter to signal)");
     return MUX_ERR_VALUE;
   }
   const int grid = grid_ctas > 0 ? grid_ctas : num_sms() * 8;

@@ -87,7 +87,7 @@ class MuxPath:
         self.flags.tensor.zero_()
         self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
                         for g in range(N_GROUPS)]
-        self.done = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.sync = torch.zeros(4, dtype=torch.int32, device=dev)  # copy counters x2
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
         # pointer tables for the copy kernels
@@ -95,6 +95,8 @@ class MuxPath:
                                     for g in range(N_GROUPS)], dev)
         self.llm_dst = _ptr_table(self.llm.ptrs, dev)
         self.enc_src = _ptr_table([t.data_ptr() for t in self.enc_out], dev)
+        self.num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.gemm_ctas = 0  # 0: one CTA per SM; plan_ahead() leaves one SM to the planner
         self.flag_ptrs = _ptr_table(self.flags.ptrs, dev)
         self._arena_tables: dict = {}
         self._plan: Plan | None = None
@@ -138,6 +140,43 @@ class MuxPath:
         self._plan = plan_step(dtab, cfg, self._plan, stream)
         return self._plan
 
+    # ------------------------------------------------------- planner pipelining
+    # The plan of step k+1 needs only metadata, so it runs on a high-priority
+    # side stream while step k's rows move; two plan buffers alternate.
+    def _ensure_ring(self):
+        if getattr(self, "_ring", None) is None:
+            self._side = torch.cuda.Stream(self.device, priority=-1)
+            self._ring = [None, None]
+            self._ready = [torch.cuda.Event(), torch.cuda.Event()]
+            self._freed = [None, None]
+
+    def plan_ahead(self, dtab: DeviceTable, slot: int, after=None) -> Plan:
+        """Plan `dtab` into ring slot 0/1 on the side stream.  `after`: an
+        event the plan must follow (e.g. the step-table upload)."""
+        self._ensure_ring()
+        self.gemm_ctas = self.num_sms - 1
+        side = self._side
+        if self._freed[slot] is not None:
+            side.wait_event(self._freed[slot])
+        if after is not None:
+            side.wait_event(after)
+        cfg = self.cfg_for(dtab.table)
+        self._ring[slot] = plan_step(dtab, cfg, self._ring[slot], side)
+        self._ready[slot].record(side)
+        return self._ring[slot]
+
+    def run_planned(self, slot: int, arenas, stream=None):
+        """Dispatch + return of the plan in ring `slot` on the main stream."""
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        main.wait_event(self._ready[slot])
+        p = self._ring[slot]
+        self.dispatch(p, arenas, main)
+        self.return_scatter(p, main)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self._freed[slot] = ev
+        return p
+
     def _arena_table(self, arenas) -> torch.Tensor:
         """Device table of loader-arena pointers, cached per arena set (no sync
         once warm)."""
@@ -153,11 +192,12 @@ class MuxPath:
         s = _stream_ptr(stream)
         if self.world == 1:
             _lib.check(L.mux_segcopy(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
-                                     dst.data_ptr(), 0, s), "mux_segcopy")
+                                     dst.data_ptr(), 0, self.sync[2 * which:].data_ptr(), s),
+                       "mux_segcopy")
             return
         _lib.check(L.mux_segcopy_signal(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
                                         dst.data_ptr(), 0, self.flag_ptrs.data_ptr(),
-                                        self.done[which:].data_ptr(), self.epoch_ctr.data_ptr(),
+                                        self.sync[2 * which:].data_ptr(), self.epoch_ctr.data_ptr(),
                                         s), "mux_segcopy_signal")
         _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch_ctr.data_ptr(),
                               self.timeout_ms, self.wait_err.data_ptr(), s), "mux_wait")
@@ -195,8 +235,8 @@ class MuxPath:
             _lib.check(L.mux_proj_scatter_dev(self.enc_out[g].data_ptr(), self.weight[g].data_ptr(),
                                               0 if b is None else b.data_ptr(), self.max_rows,
                                               m_dev, self.d_enc[g], self.d_llm,
-                                              self.row_dst.data_ptr(), self.llm_dst.data_ptr(), 0,
-                                              s), "mux_proj_scatter_dev")
+                                              self.row_dst.data_ptr(), self.llm_dst.data_ptr(),
+                                              self.gemm_ctas, s), "mux_proj_scatter_dev")
         if self.world > 1:
             _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(),
                                     self.epoch_ctr.data_ptr(), s), "mux_signal")
