@@ -36,16 +36,28 @@ __device__ __forceinline__ uint2 ld_stream2(const uint2* p) {
   return r;
 }
 
+__device__ __forceinline__ void st_u4(uint4* p, const uint4& v) { *p = v; }
+
 // Block-cooperative copy of n bytes; src, dst and n are multiples of 8.
+// After an optional 8-byte head the destination is 16-byte aligned.  If the
+// source is then 16-byte aligned too, 128-bit loads/stores stream straight
+// through; otherwise (source 8 bytes off, e.g. 1176-byte rows starting at an
+// odd row) each lane loads one aligned 16-byte source word and builds its
+// destination word from its own high half and its right neighbour's low half
+// (warp shuffle), so both sides still move 128 bits per access.
 __device__ __forceinline__ void copy_block(char* dst, const char* src, int64_t n) {
-  const int tid = threadIdx.x;
-  if ((((uintptr_t)src ^ (uintptr_t)dst) & 15) == 0) {
-    int64_t head = (16 - ((uintptr_t)src & 15)) & 15;
-    if (head > n) head = n;
-    if (head && tid == 0) *reinterpret_cast<uint2*>(dst) = ld_stream2(reinterpret_cast<const uint2*>(src));
-    const uint4* s = reinterpret_cast<const uint4*>(src + head);
-    uint4* d = reinterpret_cast<uint4*>(dst + head);
-    const int64_t n16 = (n - head) >> 4;
+  const int tid = threadIdx.x, lane = tid & 31;
+  int64_t head = (16 - ((uintptr_t)dst & 15)) & 15;  // 0 or 8
+  if (head > n) head = n;
+  if (head && tid == 0)
+    *reinterpret_cast<uint2*>(dst) = ld_stream2(reinterpret_cast<const uint2*>(src));
+  dst += head;
+  src += head;
+  n -= head;
+  const int64_t n16 = n >> 4;
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  if (((uintptr_t)src & 15) == 0) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
     int64_t i = tid;
     for (; i + (kCopyUnroll - 1) * kCopyThreads < n16; i += kCopyUnroll * kCopyThreads) {
       uint4 v[kCopyUnroll];
@@ -55,23 +67,45 @@ __device__ __forceinline__ void copy_block(char* dst, const char* src, int64_t n
       for (int u = 0; u < kCopyUnroll; ++u) d[i + u * kCopyThreads] = v[u];
     }
     for (; i < n16; i += kCopyThreads) d[i] = ld_stream(s + i);
-    const int64_t done = head + (n16 << 4);
-    if (done < n && tid == 0)
-      *reinterpret_cast<uint2*>(dst + done) = ld_stream2(reinterpret_cast<const uint2*>(src + done));
   } else {
-    const uint2* s = reinterpret_cast<const uint2*>(src);
-    uint2* d = reinterpret_cast<uint2*>(dst);
-    const int64_t n8 = n >> 3;
-    int64_t i = tid;
-    for (; i + (kCopyUnroll - 1) * kCopyThreads < n8; i += kCopyUnroll * kCopyThreads) {
-      uint2 v[kCopyUnroll];
+    // source word A[k] = 16 aligned bytes at src - 8 + 16k; dst word k takes
+    // A[k].hi and A[k+1].lo.  Warps cover contiguous k so lane+1 holds A[k+1].
+    const uint4* A = reinterpret_cast<const uint4*>(src - 8);
+    constexpr int U = 4;
+    for (int64_t base = 0; base < n16; base += U * kCopyThreads) {
+      uint4 v[U];
+      uint2 extra[U];
 #pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u) v[u] = ld_stream2(s + i + u * kCopyThreads);
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = base + u * kCopyThreads + tid;
+        // A[k] for k < n16 is fully inside the source (its low half is the
+        // previous dst word's tail); only the low half of A[n16] is read.
+        v[u] = k < n16 ? ld_stream(A + k) : make_uint4(0, 0, 0, 0);
+        extra[u] = make_uint2(0, 0);
+        if (lane == 31 && k + 1 <= n16)
+          extra[u] = ld_stream2(reinterpret_cast<const uint2*>(A + k + 1));
+      }
 #pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u) d[i + u * kCopyThreads] = v[u];
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = base + u * kCopyThreads + tid;
+        uint32_t nx = __shfl_down_sync(MUX_FULL, v[u].x, 1);
+        uint32_t ny = __shfl_down_sync(MUX_FULL, v[u].y, 1);
+        if (lane == 31) {
+          nx = extra[u].x;
+          ny = extra[u].y;
+        } else if (k + 1 == n16) {  // neighbour is past the end: A[n16].lo
+          const uint2 t = ld_stream2(reinterpret_cast<const uint2*>(A + k + 1));
+          nx = t.x;
+          ny = t.y;
+        }
+        if (k < n16) st_u4(d + k, make_uint4(v[u].z, v[u].w, nx, ny));
+      }
     }
-    for (; i < n8; i += kCopyThreads) d[i] = ld_stream2(s + i);
   }
+  const int64_t done = n16 << 4;
+  if (done < n && tid == 0)
+    *reinterpret_cast<uint2*>(dst + done) =
+        ld_stream2(reinterpret_cast<const uint2*>(src + done));
 }
 
 struct SegArgs {

@@ -26,7 +26,7 @@ import ctypes as C
 import torch
 
 from . import _lib
-from .planner import DeviceTable, Plan, StepTable, make_cfg, plan_step, _stream_ptr
+from .planner import DeviceTable, Plan, StepTable, layout_of, make_cfg, plan_step, _stream_ptr
 
 N_GROUPS = _lib.N_GROUPS
 
@@ -244,6 +244,63 @@ class MuxPath:
                                   self.epoch_ctr.data_ptr(), self.timeout_ms,
                                   self.wait_err.data_ptr(), s), "mux_wait")
 
+    # ------------------------------------------------------------ CUDA graphs
+    def capture_steps(self, dtabs, arenas_list):
+        """One CUDA graph per distinct step i: (plan of step i+1 on the side
+        stream) overlapped with (dispatch + return/scatter of step i).  Replay
+        with `StepGraphs.replay(k)`; every kernel of the pipelined step is a
+        graph node, so the host issues one launch per step."""
+        return StepGraphs(self, dtabs, arenas_list)
+
     def check_wait(self):
         if int(self.wait_err.item()):
             raise RuntimeError("cross-GPU completion flag wait timed out")
+
+
+class StepGraphs:
+    """Captured pipelined steps (see MuxPath.capture_steps)."""
+
+    def __init__(self, path: MuxPath, dtabs, arenas_list):
+        n = len(dtabs)
+        if n % 2:
+            raise ValueError("capture an even number of distinct steps (two plan buffers)")
+        path._ensure_ring()
+        path.gemm_ctas = path.num_sms - 1
+        dev = path.device
+        self.path, self.n = path, n
+        cfgs = [path.cfg_for(d.table) for d in dtabs]
+        biggest = max(layout_of(c).total for c in cfgs)
+        self.blobs = [torch.zeros(biggest, dtype=torch.uint8, device=dev) for _ in range(2)]
+        plans = [Plan(cfgs[i], dev, self.blobs[i % 2]) for i in range(n)]
+        self.plans = plans
+        side = path._side
+        # eager pass: caches pointer tables / kernel attributes, checks every plan
+        for i in range(n):
+            plan_step(dtabs[i], cfgs[i], plans[i])
+            plans[i].check(dtabs[i].table)
+            path.dispatch(plans[i], arenas_list[i])
+            path.return_scatter(plans[i])
+        torch.cuda.synchronize(dev)
+        self.graphs = []
+        cap = torch.cuda.Stream(dev)
+        for i in range(n):
+            j = (i + 1) % n
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                main = torch.cuda.current_stream(dev)
+                side.wait_stream(main)
+                plan_step(dtabs[j], cfgs[j], plans[j], side)
+                path.dispatch(plans[i], arenas_list[i], main)
+                path.return_scatter(plans[i], main)
+                main.wait_stream(side)
+            self.graphs.append(g)
+        self.dtabs, self.cfgs = dtabs, cfgs
+
+    def prime(self, k: int, stream=None):
+        """Plan step k (each graph plans step i+1 while running step i), so a
+        replay sequence starting at k must be primed with step k's plan."""
+        i = k % self.n
+        plan_step(self.dtabs[i], self.cfgs[i], self.plans[i], stream)
+
+    def replay(self, k: int):
+        self.graphs[k % self.n].replay()
