@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--stages", action="store_true", help="per-stage timing breakdown")
     ap.add_argument("--pipeline", type=int, default=1,
                     help="1: plan step k+1 on a side stream during step k (default)")
+    ap.add_argument("--hang-dump", type=float, default=0.0,
+                    help="dump Python stacks after this many seconds (debug)")
     ap.add_argument("--graphs", type=int, default=0,
                     help="1: replay one captured CUDA graph per pipelined step")
     return ap.parse_args()
@@ -310,7 +312,10 @@ def run_ours(args):
         torch.cuda.synchronize()
         # untimed soak (~100 ms) so the clock record covers a loaded GPU
         est = max(t0.elapsed_time(t1) / max(args.warmup, 1), 0.01)
-        run_steps(0, int(min(100.0 / est, 5000)))
+        n_soak = torch.tensor([int(min(100.0 / est, 5000))], device=dev)
+        if world > 1:  # every rank must run the same number of exchanges
+            dist.all_reduce(n_soak, op=dist.ReduceOp.MIN)
+        run_steps(0, int(n_soak.item()))
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -613,6 +618,9 @@ def cpu_baseline_world(name, table, world, projector):
 
 def main():
     args = parse()
+    if args.hang_dump > 0:
+        import faulthandler
+        faulthandler.dump_traceback_later(args.hang_dump, exit=False)
     if args.impl == "reference":
         run_reference(args)
     else:
