@@ -160,6 +160,12 @@ int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                        uint64_t* const* flags_peers, uint32_t* sync, uint64_t* epoch_ctr,
                        void* stream);
 
+/* One contiguous 8-byte-aligned byte range with the same copy engine as
+ * mux_segcopy (local or NVLink-peer dst/src); used by the NVLink probe. */
+int mux_copy_bytes(void* dst, const void* src, int64_t n, int32_t grid_ctas, void* stream);
+/* cudaMemcpyAsync(cudaMemcpyDefault): the copy-engine comparator of the probe. */
+int mux_memcpy_async(void* dst, const void* src, int64_t n, void* stream);
+
 /* Cross-GPU completion flags.  flags_peers: device array of `world` device
  * pointers to each rank's uint64 flag array (world entries each).  signal
  * advances the device epoch counter (e = ++*epoch_ctr) and stores e into

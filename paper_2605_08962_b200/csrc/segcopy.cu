@@ -194,6 +194,14 @@ __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int sm
   }
 }
 
+// One contiguous byte range (probe / utility): grid-stride 32 KiB blocks.
+__global__ void __launch_bounds__(kCopyThreads) copy_bytes_kernel(char* dst, const char* src,
+                                                                  int64_t n) {
+  const int64_t CH = kDefaultChunkBytes;
+  for (int64_t lo = (int64_t)blockIdx.x * CH; lo < n; lo += (int64_t)gridDim.x * CH)
+    copy_block(dst + lo, src + lo, n - lo < CH ? n - lo : CH);
+}
+
 __global__ void signal_kernel(int me, int world, uint64_t* const* flags_peers,
                               uint64_t* epoch_ctr) {
   const int r = threadIdx.x;
@@ -393,5 +401,25 @@ extern "C" int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_
   Plan p = make_plan_const(plan, L);
   return_rows_kernel<<<256, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, group, row_dst, n_rows);
   MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_copy_bytes(void* dst, const void* src, int64_t n, int32_t grid_ctas,
+                              void* stream) {
+  if ((((uintptr_t)dst | (uintptr_t)src | (uintptr_t)n) & 7) != 0) {
+    set_error("mux_copy_bytes needs 8-byte aligned pointers and size");
+    return MUX_ERR_VALUE;
+  }
+  if (n == 0) return MUX_OK;
+  const int grid = grid_ctas > 0 ? grid_ctas : num_sms() * 8;
+  copy_bytes_kernel<<<grid, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<char*>(dst), static_cast<const char*>(src), n);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_memcpy_async(void* dst, const void* src, int64_t n, void* stream) {
+  MUX_CUDA(cudaMemcpyAsync(dst, src, (size_t)n, cudaMemcpyDefault,
+                           static_cast<cudaStream_t>(stream)));
   return MUX_OK;
 }
