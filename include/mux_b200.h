@@ -68,7 +68,13 @@ extern "C" {
 #define MUX_H_RETURN_REMOTE 11   /* return bytes leaving rank `me`             */
 #define MUX_H_RECV_ROWS0 12   /* rows received by `me`, group 0 / group 1      */
 #define MUX_H_RECV_ROWS1 13
+#define MUX_H_STAGE_ROWS0 14  /* rows staged on `me` for its projector, group 0/1 */
+#define MUX_H_STAGE_ROWS1 15
 #define MUX_H_SLOTS 32
+
+#define MUX_RET_FINAL 0  /* return rows go to their final packed-LLM rows           */
+#define MUX_RET_STAGED 1 /* return d_enc rows to the owner's per-group staging      */
+                         /* buffer (LLM order); the owner then projects locally     */
 
 typedef struct {
   int32_t S;            /* samples in the step table                        */
@@ -84,6 +90,7 @@ typedef struct {
   int32_t row_bytes_in[MUX_N_GROUPS];  /* loader row bytes per group        */
   int32_t row_bytes_ret[MUX_N_GROUPS]; /* returned row bytes per group      */
   int32_t chunk_bytes;  /* copy work unit (0 = default 32 KiB)              */
+  int32_t ret_mode;     /* MUX_RET_FINAL | MUX_RET_STAGED (sp == 1 only)      */
 } mux_plan_cfg;
 
 /* Byte offsets of every array inside the plan buffer (one device blob). */
@@ -91,7 +98,7 @@ typedef struct {
   int64_t header;                                   /* int64[MUX_H_SLOTS] */
   int64_t sync;     /* uint32 ticket; must be zero when the blob is first used */
   int64_t seq, off, span, origin, origin_pos, group, enc; /* int32[S]      */
-  int64_t arena_off, enc_off;                       /* int64[S]           */
+  int64_t arena_off, enc_off, stage_off;            /* int64[S]           */
   int64_t llm_rank, llm_row;                        /* int32/int64[S]     */
   int64_t bin_fill, bin_nspan, bin_of;              /* int32[S] (scratch) */
   int64_t chunk_nbins, chunk_err;                   /* int32[n_chunks]    */
@@ -99,7 +106,7 @@ typedef struct {
   int64_t cu;                                       /* int32[gbs+1]       */
   int64_t shard_len, shard_start;                   /* int32[gbs*sp]      */
   int64_t row_base;                                 /* int64[gbs*sp]      */
-  int64_t arena_rows, recv_rows;                    /* int64[world*2]     */
+  int64_t arena_rows, recv_rows, stage_rows;        /* int64[world*2]     */
   int64_t llm_rows;                                 /* int64[world]       */
   int64_t order, scratch_a, scratch_b;              /* int32[S] (scratch) */
   /* dispatch segments (rank me): rows from arena[group] to recv[group]@enc */
@@ -188,6 +195,12 @@ int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, const int64_t
  * destination table: row_dst[src_row] = (dst_rank << 40) | dst_row. */
 int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_t group,
                     int64_t* row_dst, int64_t n_rows, void* stream);
+
+/* MUX_RET_STAGED: per-row destination of the owner's staging rows of
+ * `group`: row_dst[stage_off + t] = (me << 40) | (llm_row + t).  lens: the
+ * step table's int32 lengths (device). */
+int mux_stage_rows(const mux_plan_cfg* cfg, const void* plan, const int32_t* lens,
+                   int32_t group, int64_t* row_dst, int64_t n_rows, void* stream);
 
 /* Projector fused with the scatter: for m < M,
  *   out_rank[row_dst[m] >> 40][row_dst[m] & (2^40-1), :] =

@@ -20,6 +20,8 @@ N_GROUPS = 2
 H_STATUS, H_ERR_INDEX, H_N_SEQ, H_N_DISPATCH, H_N_RETURN = 0, 1, 2, 3, 4
 H_DISPATCH_CHUNKS, H_RETURN_CHUNKS, H_DISPATCH_BYTES, H_RETURN_BYTES = 5, 6, 7, 8
 H_N_BATCH, H_DISPATCH_REMOTE, H_RETURN_REMOTE, H_RECV_ROWS0, H_RECV_ROWS1 = 9, 10, 11, 12, 13
+H_STAGE_ROWS0, H_STAGE_ROWS1 = 14, 15
+RET_FINAL, RET_STAGED = 0, 1
 H_SLOTS = 32
 
 
@@ -28,14 +30,14 @@ class PlanCfg(C.Structure):
         "S", "n_carry", "n_carry_seqs", "n_chunks", "capacity", "gbs", "dp", "sp", "world",
         "mbs", "method", "pooled", "me", "mode")] + [
         ("row_bytes_in", C.c_int32 * N_GROUPS), ("row_bytes_ret", C.c_int32 * N_GROUPS),
-        ("chunk_bytes", C.c_int32)]
+        ("chunk_bytes", C.c_int32), ("ret_mode", C.c_int32)]
 
 
 LAYOUT_FIELDS = (
     "header", "sync", "seq", "off", "span", "origin", "origin_pos", "group", "enc", "arena_off",
-    "enc_off", "llm_rank", "llm_row", "bin_fill", "bin_nspan", "bin_of", "chunk_nbins",
+    "enc_off", "stage_off", "llm_rank", "llm_row", "bin_fill", "bin_nspan", "bin_of", "chunk_nbins",
     "chunk_err", "fills", "nspans", "cu", "shard_len", "shard_start", "row_base", "arena_rows",
-    "recv_rows", "llm_rows", "order", "scratch_a", "scratch_b", "dseg_src_row", "dseg_dst_row",
+    "recv_rows", "stage_rows", "llm_rows", "order", "scratch_a", "scratch_b", "dseg_src_row", "dseg_dst_row",
     "dseg_rows", "dseg_group", "dseg_dst_rank", "dseg_chunk0", "rseg_src_row", "rseg_dst_row",
     "rseg_rows", "rseg_group", "rseg_dst_rank", "rseg_chunk0", "total")
 
@@ -64,6 +66,7 @@ _SIGS = [
     ("mux_encoder_standin", C.c_int, [C.POINTER(PlanCfg), _P, _P, _P, C.c_int32, C.c_int32, _P,
                                       _P]),
     ("mux_return_rows", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, C.c_int64, _P]),
+    ("mux_stage_rows", C.c_int, [C.POINTER(PlanCfg), _P, _P, C.c_int32, _P, C.c_int64, _P]),
     ("mux_proj_scatter", C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P,
                                    C.c_int32, _P]),
     ("mux_proj_scatter_dev", C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P,

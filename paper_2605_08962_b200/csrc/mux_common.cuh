@@ -110,10 +110,10 @@ struct Plan {
   int64_t* hdr;
   uint32_t* ticket;  // last-CTA ticket of plan_kernel (zero between launches)
   int32_t *seq, *off, *span, *origin, *origin_pos, *group, *enc, *llm_rank;
-  int64_t *arena_off, *enc_off, *llm_row;
+  int64_t *arena_off, *enc_off, *stage_off, *llm_row;
   int32_t *bin_fill, *bin_nspan, *bin_of, *chunk_nbins, *chunk_err, *fills, *nspans, *cu;
   int32_t *shard_len, *shard_start;
-  int64_t *row_base, *arena_rows, *recv_rows, *llm_rows;
+  int64_t *row_base, *arena_rows, *recv_rows, *stage_rows, *llm_rows;
   int32_t *order, *scratch_a, *scratch_b;
   int64_t *dsrc, *ddst, *drows, *dchunk0;
   int32_t *dgroup, *drank;

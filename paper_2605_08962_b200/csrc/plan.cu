@@ -58,6 +58,10 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
       set_error("gbs x sp exceeds the device planner limit 4096");
       return MUX_ERR_VALUE;
     }
+    if (c.ret_mode == MUX_RET_STAGED && c.sp != 1) {
+      set_error("staged projector return needs Ulysses sp == 1 (got %d)", c.sp);
+      return MUX_ERR_VALUE;
+    }
   }
   const int64_t S = c.S > 0 ? c.S : 1;
   const int64_t nch = c.n_chunks > 0 ? c.n_chunks : 1;
@@ -82,6 +86,7 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->enc = take(4 * S);
   L->arena_off = take(8 * S);
   L->enc_off = take(8 * S);
+  L->stage_off = take(8 * S);
   L->llm_rank = take(4 * S);
   L->llm_row = take(8 * S);
   L->bin_fill = take(4 * S);
@@ -97,6 +102,7 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->row_base = take(8 * gb);
   L->arena_rows = take(8 * W * MUX_N_GROUPS);
   L->recv_rows = take(8 * W * MUX_N_GROUPS);
+  L->stage_rows = take(8 * W * MUX_N_GROUPS);
   L->llm_rows = take(8 * W);
   L->order = take(4 * S);
   L->scratch_a = take(4 * S);
@@ -135,6 +141,7 @@ Plan make_plan(void* b, const mux_plan_layout& L) {
   p.enc = at<int32_t>(b, L.enc);
   p.arena_off = at<int64_t>(b, L.arena_off);
   p.enc_off = at<int64_t>(b, L.enc_off);
+  p.stage_off = at<int64_t>(b, L.stage_off);
   p.llm_rank = at<int32_t>(b, L.llm_rank);
   p.llm_row = at<int64_t>(b, L.llm_row);
   p.bin_fill = at<int32_t>(b, L.bin_fill);
@@ -150,6 +157,7 @@ Plan make_plan(void* b, const mux_plan_layout& L) {
   p.row_base = at<int64_t>(b, L.row_base);
   p.arena_rows = at<int64_t>(b, L.arena_rows);
   p.recv_rows = at<int64_t>(b, L.recv_rows);
+  p.stage_rows = at<int64_t>(b, L.stage_rows);
   p.llm_rows = at<int64_t>(b, L.llm_rows);
   p.order = at<int32_t>(b, L.order);
   p.scratch_a = at<int32_t>(b, L.scratch_a);
@@ -935,6 +943,45 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
   for (int x = tid; x < W * MUX_N_GROUPS; x += nt) p.recv_rows[x] = s_carry[x];
   __syncthreads();
 
+  // ---- H2. staged return (projector, sp == 1): owner-side staging rows per
+  //          (owner rank, group), in LLM order = (origin, origin_pos) order ----
+  if (cfg.ret_mode == MUX_RET_STAGED) {
+    if (tid < kMaxKeys) s_carry[tid] = 0;
+    __syncthreads();
+    for (int base = 0; base < S; base += nt) {  // batch samples per origin
+      const int i = base + tid;
+      const bool b = i < S && w.seq[i] < gbs;
+      multi_scan(b ? w.org[i] : -1, 1, W, s_wk, s_carry);
+    }
+    if (tid == 0) {
+      int64_t acc = 0;
+      for (int r = 0; r < W; ++r) {
+        const int64_t c = s_carry[r];
+        s_carry[r] = acc;
+        acc += c;
+      }
+      s_misc[2] = (int)acc;
+    }
+    __syncthreads();
+    for (int i = tid; i < S; i += nt)  // w.order <- batch samples by (origin, origin_pos)
+      if (w.seq[i] < gbs) w.order[s_carry[w.org[i]] + w.opos[i]] = i;
+    __syncthreads();
+    const int nb = s_misc[2];
+    if (tid < kMaxKeys) s_carry[tid] = 0;
+    __syncthreads();
+    for (int base = 0; base < nb; base += nt) {
+      const int t = base + tid;
+      const int i = t < nb ? w.order[t] : 0;
+      const bool e = t < nb && w.grp[i] >= 0;
+      const int64_t pre = multi_scan(e ? w.org[i] * MUX_N_GROUPS + w.grp[i] : -1,
+                                     e ? w.len[i] : 0, W * MUX_N_GROUPS, s_wk, s_carry);
+      if (e) p.stage_off[i] = pre;
+      else if (t < nb) p.stage_off[i] = -1;
+    }
+    for (int x = tid; x < W * MUX_N_GROUPS; x += nt) p.stage_rows[x] = s_carry[x];
+    __syncthreads();
+  }
+
   // ---- I. LLM positions, return pieces and segment tables of rank `me` -------
   stamp(p, 24);
   const int me = cfg.me;
@@ -1004,7 +1051,9 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
       const int dst = (q / P) * sp + kk;
       const int64_t nb = (int64_t)n * cfg.row_bytes_ret[g];
       p.rsrc[slot] = w.eoff[i] + t;
-      p.rdst[slot] = p.row_base[q * sp + kk] + pos - s_sstart[q * sp + kk];
+      p.rdst[slot] = cfg.ret_mode == MUX_RET_STAGED
+                         ? p.stage_off[i] + t
+                         : p.row_base[q * sp + kk] + pos - s_sstart[q * sp + kk];
       p.rrows[slot] = n;
       p.rgroup[slot] = g;
       p.rrank[slot] = dst;
@@ -1037,6 +1086,9 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
       p.hdr[MUX_H_N_RETURN] = rcarry;
       p.hdr[MUX_H_RECV_ROWS0] = p.recv_rows[me * MUX_N_GROUPS + 0];
       p.hdr[MUX_H_RECV_ROWS1] = p.recv_rows[me * MUX_N_GROUPS + 1];
+      const bool st = cfg.ret_mode == MUX_RET_STAGED;
+      p.hdr[MUX_H_STAGE_ROWS0] = st ? p.stage_rows[me * MUX_N_GROUPS + 0] : 0;
+      p.hdr[MUX_H_STAGE_ROWS1] = st ? p.stage_rows[me * MUX_N_GROUPS + 1] : 0;
     }
   }
   emit(cfg, p, w, small, n_seq, true);

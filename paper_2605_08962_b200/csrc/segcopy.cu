@@ -293,6 +293,18 @@ __global__ void return_rows_kernel(Plan p, int group, int64_t* row_dst, int64_t 
   }
 }
 
+// Staged projector return: row_dst of the owner's staging rows of `group`.
+__global__ void stage_rows_kernel(Plan p, const int32_t* lens, int S, int me, int group,
+                                  int64_t* row_dst, int64_t n_rows) {
+  for (int i = blockIdx.x; i < S; i += gridDim.x) {
+    if (p.origin[i] != me || p.group[i] != group || p.enc[i] < 0) continue;
+    const int64_t s0 = p.stage_off[i], l0 = p.llm_row[i];
+    const int64_t tag = (int64_t)me << 40;
+    for (int64_t t = threadIdx.x; t < lens[i]; t += blockDim.x)
+      if (s0 + t < n_rows) row_dst[s0 + t] = tag | (l0 + t);
+  }
+}
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -336,7 +348,7 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
   a.chunk_bytes = cfg->chunk_bytes > 0 ? cfg->chunk_bytes : kDefaultChunkBytes;
   for (int g = 0; g < MUX_N_GROUPS; ++g)
     a.row_bytes[g] = ret ? cfg->row_bytes_ret[g] : cfg->row_bytes_in[g];
-  a.per_group_dst = ret ? 0 : 1;
+  a.per_group_dst = (!ret || cfg->ret_mode == MUX_RET_STAGED) ? 1 : 0;
   a.src_bases = src_bases;
   a.dst_bases = dst_bases;
   a.flags_peers = flags_peers;
@@ -421,5 +433,23 @@ extern "C" int mux_copy_bytes(void* dst, const void* src, int64_t n, int32_t gri
 extern "C" int mux_memcpy_async(void* dst, const void* src, int64_t n, void* stream) {
   MUX_CUDA(cudaMemcpyAsync(dst, src, (size_t)n, cudaMemcpyDefault,
                            static_cast<cudaStream_t>(stream)));
+  return MUX_OK;
+}
+
+extern "C" int mux_stage_rows(const mux_plan_cfg* cfg, const void* plan, const int32_t* lens,
+                              int32_t group, int64_t* row_dst, int64_t n_rows, void* stream) {
+  if (cfg->ret_mode != MUX_RET_STAGED) {
+    set_error("mux_stage_rows needs a plan made with ret_mode MUX_RET_STAGED");
+    return MUX_ERR_VALUE;
+  }
+  mux_plan_layout L;
+  int st = mux_plan_layout_of(cfg, &L);
+  if (st) return st;
+  Plan p = make_plan_const(plan, L);
+  const int grid = cfg->S > 0 ? (cfg->S < 1024 ? cfg->S : 1024) : 1;
+  stage_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, lens, cfg->S,
+                                                                         cfg->me, group,
+                                                                         row_dst, n_rows);
+  MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

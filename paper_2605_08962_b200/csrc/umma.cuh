@@ -61,6 +61,26 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// bulk (non-tensor) smem -> global copy through the TMA engine; dst may be a
+// local or NVLink-peer global address.  bytes % 16 == 0, both 16-B aligned.
+__device__ __forceinline__ void bulk_store(void* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(ssrc), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---- tcgen05 -------------------------------------------------------------------
 // Shared-memory matrix descriptor, K-major, 128-byte swizzle: 8-row x 128-B
 // atoms stacked at SBO = 1024 B; LBO unused (1); version 1 (sm_100).

@@ -77,12 +77,18 @@ class MuxPath:
         self.group = group
         self.timeout_ms = wait_timeout_ms
         self.d_ret = tuple(d_enc) if projector else (d_llm, d_llm)
+        # projector across GPUs: return the narrow d_enc rows to the LLM owner's
+        # staging window, then project locally (3.2x fewer NVLink bytes than
+        # returning d_llm rows); on one GPU the GEMM reads the encoder rows directly
+        self.ret_mode = _lib.RET_STAGED if projector and world > 1 else _lib.RET_FINAL
         rows = max_rows or gbs * capacity                       # all batch tokens
         llm_rows = (gbs // dp) * capacity // sp + gbs // dp + 1  # one rank's shards
         self.max_rows, self.max_llm_rows = rows, llm_rows
         dev = self.device
         self.recv = [_Window(rows * d_in[g] * 2, dev, group, world) for g in range(N_GROUPS)]
         self.llm = _Window(llm_rows * d_llm * 2, dev, group, world)
+        self.stage = [_Window(llm_rows * d_enc[g] * 2, dev, group, world) for g in range(N_GROUPS)] \
+            if self.ret_mode == _lib.RET_STAGED else None
         self.flags = _Window(8 * world, dev, group, world)
         self.flags.tensor.zero_()
         self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
@@ -94,6 +100,9 @@ class MuxPath:
         self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
                                     for g in range(N_GROUPS)], dev)
         self.llm_dst = _ptr_table(self.llm.ptrs, dev)
+        if self.stage is not None:
+            self.stage_dst = _ptr_table([self.stage[g].ptrs[r] for r in range(world)
+                                         for g in range(N_GROUPS)], dev)
         self.enc_src = _ptr_table([t.data_ptr() for t in self.enc_out], dev)
         self.num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.gemm_ctas = 0  # 0: one CTA per SM; plan_ahead() leaves one SM to the planner
@@ -106,7 +115,7 @@ class MuxPath:
         if projector:
             self.weight = [None] * N_GROUPS
             self.bias = [None] * N_GROUPS
-            self.row_dst = torch.empty(rows, dtype=torch.int64, device=dev)
+            self.row_dst = torch.empty(max(rows, llm_rows), dtype=torch.int64, device=dev)
 
     # ------------------------------------------------------------------ setup
     def set_projector(self, group: int, weight: torch.Tensor, bias: torch.Tensor | None = None):
@@ -120,7 +129,7 @@ class MuxPath:
         return make_cfg(table, self.capacity, self.gbs, self.dp, self.sp, self.world, 1,
                         self.method, self.pooled, self.rank,
                         row_bytes_in=tuple(2 * d for d in self.d_in),
-                        row_bytes_ret=tuple(2 * d for d in self.d_ret))
+                        row_bytes_ret=tuple(2 * d for d in self.d_ret), ret_mode=self.ret_mode)
 
     def llm_view(self, rows: int | None = None) -> torch.Tensor:
         n = self.max_llm_rows if rows is None else rows
@@ -225,6 +234,23 @@ class MuxPath:
         L = _lib.lib()
         s = _stream_ptr(stream)
         hdr = plan.ptr + plan.layout.header
+        if self.ret_mode == _lib.RET_STAGED:
+            # d_enc rows -> owner's staging window (NVLink push + flags), then local GEMM
+            self._exchange(plan, 1, self.enc_src, self.stage_dst, stream)
+            for g in range(N_GROUPS):
+                if self.weight[g] is None:
+                    continue
+                _lib.check(L.mux_stage_rows(C.byref(plan.cfg), plan.ptr, plan.lens_ptr, g,
+                                            self.row_dst.data_ptr(), self.max_llm_rows, s),
+                           "mux_stage_rows")
+                b = self.bias[g]
+                _lib.check(L.mux_proj_scatter_dev(
+                    self.stage[g].tensor.data_ptr(), self.weight[g].data_ptr(),
+                    0 if b is None else b.data_ptr(), self.max_llm_rows,
+                    hdr + 8 * (_lib.H_STAGE_ROWS0 + g), self.d_enc[g], self.d_llm,
+                    self.row_dst.data_ptr(), self.llm_dst.data_ptr(), self.gemm_ctas, s),
+                    "mux_proj_scatter_dev")
+            return
         for g in range(N_GROUPS):
             if self.weight[g] is None:
                 continue
@@ -237,7 +263,7 @@ class MuxPath:
                                               m_dev, self.d_enc[g], self.d_llm,
                                               self.row_dst.data_ptr(), self.llm_dst.data_ptr(),
                                               self.gemm_ctas, s), "mux_proj_scatter_dev")
-        if self.world > 1:
+        if self.world > 1:  # (direct mode across GPUs: GEMM stored to peers)
             _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(),
                                     self.epoch_ctr.data_ptr(), s), "mux_signal")
             _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(),

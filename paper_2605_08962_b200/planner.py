@@ -116,7 +116,8 @@ class DeviceTable:
 def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int = 1,
              world: int = 1, mbs: int = 1, method: str = "lpt", pooled: bool = False,
              me: int = 0, mode: int = _lib.MODE_STEP, row_bytes_in=(1176, 1024),
-             row_bytes_ret=(8192, 8192), chunk_bytes: int = DEFAULT_CHUNK_BYTES) -> PlanCfg:
+             row_bytes_ret=(8192, 8192), chunk_bytes: int = DEFAULT_CHUNK_BYTES,
+             ret_mode: int = _lib.RET_FINAL) -> PlanCfg:
     if method not in METHODS:
         raise ValueError(f"unknown balance method {method!r}")
     c = PlanCfg()
@@ -128,6 +129,7 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
         c.row_bytes_in[g] = row_bytes_in[g]
         c.row_bytes_ret[g] = row_bytes_ret[g]
     c.chunk_bytes = chunk_bytes
+    c.ret_mode = ret_mode
     return c
 
 
@@ -224,6 +226,7 @@ def plan_step(dtab: DeviceTable, cfg: PlanCfg, plan: Plan | None = None, stream=
                                   dtab.chunk_off, plan.ptr, plan.blob.numel(),
                                   _stream_ptr(stream))
     _lib.check(st, "mux_plan_step")
+    plan.lens_ptr, plan.ids_ptr = dtab.lens, dtab.ids  # the table the plan was made from
     return plan
 
 

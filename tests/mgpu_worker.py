@@ -34,6 +34,7 @@ def payload(rows, width, seed):
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
     narrow = "narrow" in sys.argv
+    proj = "proj" in sys.argv
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -47,8 +48,20 @@ def main():
     d_llm = 64 if narrow else 512
     descs = owork.descs_from_config(configs.DATASETS, cfg["datasets"])
     carry, seen = None, {}
+    d_enc = (256, 256)
+    if proj and sp != 1:
+        sp, dp = 1, world
+        gbs = cfg["gbs_per_replica"] * dp
     path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
-                   d_in=d_in, d_llm=d_llm, device=dev, group=dist.group.WORLD)
+                   d_in=d_in, d_enc=d_enc, d_llm=d_llm, device=dev, group=dist.group.WORLD,
+                   projector=proj)
+    if proj:
+        gw = torch.Generator().manual_seed(9)
+        Ws = [(torch.randn(d_llm, d_enc[g], generator=gw) / d_enc[g] ** 0.5).to(torch.bfloat16)
+              for g in range(2)]
+        bs = [torch.randn(d_llm, generator=gw).to(torch.bfloat16) for g in range(2)]
+        for g in range(2):
+            path.set_projector(g, Ws[g].to(dev), bs[g].to(dev))
     fails = 0
     for step in range(3):
         _, rest, drawn, chunks = owork.generate(descs, cfg["phases"], False, step, cfg["seed"],
@@ -58,7 +71,7 @@ def main():
             seen[s[0]] = s[1]
         t = oplan.step_table(list(carry or []) if cfg["carry"] else [], drawn, chunks, seen)
         carry = rest
-        for method in ("lpt", "kk"):
+        for method in (("lpt",) if proj else ("lpt", "kk")):
             path.method = method
             o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
             arenas = [[payload(int(o["arena_rows"][r, g]), d_in[g], 1000 * step + 10 * r + g)
@@ -79,6 +92,28 @@ def main():
             path.check_wait()
             ar = [[a.view(torch.int16).numpy().view(np.uint16) for a in arenas[r]]
                   for r in range(world)]
+            if proj:  # projected rows vs a torch fp32 reference (tolerance, test_gpu_proj.py)
+                n = int(o["llm_rows"][rank])
+                got = path.llm_view(n).float()
+                ref = torch.zeros(n, d_llm, device=dev)
+                mask = torch.zeros(n, dtype=torch.bool, device=dev)
+                for (i, src, dst_rank, dst_row, rows) in o["pieces"]:
+                    if dst_rank != rank:
+                        continue
+                    g = int(o["group"][i])
+                    x = torch.from_numpy(odp.standin(int(t["ids"][i]), int(t["lens"][i]), d_enc[g])
+                                         .view(np.int16)).view(torch.bfloat16).to(dev)
+                    ref[dst_row:dst_row + rows] = x.float() @ Ws[g].to(dev).float().t() + \
+                        bs[g].to(dev).float()
+                    mask[dst_row:dst_row + rows] = True
+                err = (got - ref).abs()
+                ok = bool((err <= 2.0 ** -7 * ref.abs() + 1e-3).all()) and \
+                    bool((got[~mask] == 0).all())
+                if not ok:
+                    print(f"rank {rank} step {step}: projected rows differ", flush=True)
+                    fails += 1
+                dist.barrier()
+                continue
             recv, _, llm = odp.run_world(o, t, world, ar, d_in, (d_llm, d_llm), d_llm)
             for g in range(2):
                 n = int(o["recv_rows"][rank, g])

@@ -17,7 +17,7 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("config", ["cfg5", "cfg3", "cfg4"])
+@pytest.mark.parametrize("config", ["cfg5", "cfg3", "cfg4", "cfg2 proj"])
 def test_push_exchange_bit_exact(config):
     n = _ngpus()
     if n < 2:
@@ -27,7 +27,7 @@ def test_push_exchange_bit_exact(config):
         world = 2  # dp=2 x sp=1 fallback when sp=4 does not divide
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29611",
-           os.path.join(ROOT, "tests", "mgpu_worker.py"), config]
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), *config.split()]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
