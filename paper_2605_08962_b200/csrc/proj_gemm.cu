@@ -31,8 +31,9 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int kThreads = 192;
-constexpr int kStagingBytes = 4 * 32 * 256;  // epilogue: 4 warps x 32 rows x 256 B
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, 128 columns each
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kStagingBytes = kEpiWarps * 32 * 128;  // per warp: 32 rows x 128 B
 constexpr int kSmem = STAGES * STAGE_BYTES + 256 + kStagingBytes + 1024;
 constexpr int64_t kRowMask = (1ll << 40) - 1;
 
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * kEpiWarps);
     }
     mbar_fence_init();
   }
@@ -138,12 +139,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // Epilogue: TMEM -> registers (+bias, bf16) -> warp-private smem staging
-    // (XOR-swizzled, conflict-free) -> coalesced 256-byte row segments to the
-    // destination row, local or NVLink peer (full 128-B lines on the wire).
-    const int quarter = warp & 3;
+    // Epilogue, 8 warps: warp w drains TMEM lane quarter w%4 and one half of
+    // the tile's 256 columns, 64 columns per round: TMEM -> registers (+bias,
+    // bf16) -> warp-private smem staging (XOR-swizzled, conflict-free) ->
+    // coalesced 128-byte row segments (4 rows per store instruction) to each
+    // row's destination, local or NVLink peer.  Twice the storing warps of a
+    // 4-warp epilogue keeps more peer writes in flight.
+    const int quarter = warp & 3, colgrp = (warp - 2) >> 2;
     uint4* stage = reinterpret_cast<uint4*>(smem + STAGES * STAGE_BYTES + 256) +
-                   (warp - 2) * (32 * 16);  // [32 rows][16 x uint4] = 8 KB per warp
+                   (warp - 2) * (32 * 8);  // [32 rows][8 x uint4] = 4 KB per warp
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -153,16 +157,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (m < M) {
         const int64_t rd = row_dst[m];
         my_dst = static_cast<char*>(out_bases[rd >> 40]) +
-                 ((rd & kRowMask) * N + (int64_t)n_blk * BN) * 2;
+                 ((rd & kRowMask) * N + (int64_t)n_blk * BN + colgrp * 128) * 2;
       }
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
 #pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-#pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
+      for (int sub = 0; sub < 2; ++sub) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
           uint32_t v[32];
-          const int col = half * 128 + j * 32;
+          const int col = colgrp * 128 + sub * 64 + j * 32;
           tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + col, v);
           tmem_wait_ld();
           const int n0 = n_blk * BN + col;
@@ -179,18 +183,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            stage[lane * 16 + ((j * 4 + q) ^ (lane & 7))] =
+            stage[lane * 8 + ((j * 4 + q) ^ (lane & 7))] =
                 make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         }
         __syncwarp();
-        // two rows per iteration: lanes 0-15 row r, lanes 16-31 row r+1
-        const int sub = lane >> 4, c16 = lane & 15;
+        // four rows per store instruction: lanes 8r'..8r'+7 write row r+r'
+        const int c8 = lane & 7;
 #pragma unroll 4
-        for (int r = 0; r < 32; r += 2) {
-          const int row = r + sub;
+        for (int r = 0; r < 32; r += 4) {
+          const int row = r + (lane >> 3);
           char* d = reinterpret_cast<char*>(__shfl_sync(MUX_FULL, (unsigned long long)my_dst, row));
-          const uint4 val = stage[row * 16 + (c16 ^ (row & 7))];
-          if (d) *reinterpret_cast<uint4*>(d + half * 256 + c16 * 16) = val;
+          const uint4 val = stage[row * 8 + (c8 ^ (row & 7))];
+          if (d) *reinterpret_cast<uint4*>(d + sub * 128 + c8 * 16) = val;
         }
         __syncwarp();
       }

@@ -22,6 +22,7 @@ already knows every offset.  At world 1 the same kernels run on local pointers.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -68,7 +69,7 @@ class MuxPath:
                  rank: int = 0, method: str = "lpt", pooled: bool = False,
                  d_in=(588, 512), d_enc=(1280, 1280), d_llm: int = 4096,
                  projector: bool = False, device=None, group=None, max_rows: int | None = None,
-                 wait_timeout_ms: int = 20000):
+                 wait_timeout_ms: int = 20000, projector_return: str | None = None):
         self.capacity, self.gbs, self.dp, self.sp = capacity, gbs, dp, sp
         self.world, self.rank, self.method, self.pooled = world, rank, method, pooled
         self.d_in, self.d_enc, self.d_llm = tuple(d_in), tuple(d_enc), d_llm
@@ -77,10 +78,19 @@ class MuxPath:
         self.group = group
         self.timeout_ms = wait_timeout_ms
         self.d_ret = tuple(d_enc) if projector else (d_llm, d_llm)
-        # projector across GPUs: return the narrow d_enc rows to the LLM owner's
-        # staging window, then project locally (3.2x fewer NVLink bytes than
-        # returning d_llm rows); on one GPU the GEMM reads the encoder rows directly
-        self.ret_mode = _lib.RET_STAGED if projector and world > 1 else _lib.RET_FINAL
+        # projector across GPUs, two designs:
+        #  "fused"  (default) the GEMM runs on the encoder rank (where LPT balanced
+        #           the rows) and its epilogue bulk-stores each output row straight
+        #           into the owner's packed buffer over NVLink;
+        #  "staged" the narrow d_enc rows go to the owner's staging window (3.2x
+        #           fewer NVLink bytes), which then projects locally (its rows are
+        #           not balanced by the encoder-side LPT).
+        mode = projector_return or os.environ.get("MUX_PROJECTOR_RETURN", "fused")
+        if mode not in ("fused", "staged"):
+            raise ValueError(f"projector_return must be 'fused' or 'staged', not {mode!r}")
+        self.projector_return = mode
+        self.ret_mode = _lib.RET_STAGED if projector and world > 1 and mode == "staged" \
+            else _lib.RET_FINAL
         rows = max_rows or gbs * capacity                       # all batch tokens
         llm_rows = (gbs // dp) * capacity // sp + gbs // dp + 1  # one rank's shards
         self.max_rows, self.max_llm_rows = rows, llm_rows

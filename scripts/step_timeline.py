@@ -91,9 +91,9 @@ def main():
                 L.mux_wait(world, path.flags.tensor.data_ptr(), path.epoch_ctr.data_ptr(), 20000,
                            path.wait_err.data_ptr(), s)
                 marks.append(("return wait", ev()))
-        elif world == 1:
+        elif world == 1 or path.ret_mode == _lib.RET_FINAL:
             path.return_scatter(p, st)
-            marks.append(("return_rows + projector GEMM", ev()))
+            marks.append(("return_rows + projector GEMM (+signal/wait)", ev()))
         else:
             L.mux_segcopy_signal(C.byref(p.cfg), p.ptr, 1, path.enc_src.data_ptr(),
                                  path.stage_dst.data_ptr(), 0, path.flag_ptrs.data_ptr(),

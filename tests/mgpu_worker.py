@@ -54,7 +54,7 @@ def main():
         gbs = cfg["gbs_per_replica"] * dp
     path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
                    d_in=d_in, d_enc=d_enc, d_llm=d_llm, device=dev, group=dist.group.WORLD,
-                   projector=proj)
+                   projector=proj, projector_return="staged" if "staged" in sys.argv else "fused")
     if proj:
         gw = torch.Generator().manual_seed(9)
         Ws = [(torch.randn(d_llm, d_enc[g], generator=gw) / d_enc[g] ** 0.5).to(torch.bfloat16)
