@@ -280,22 +280,21 @@ def run_ours(args):
             for k in range(n):
                 one_step(k0 + k, timed_dom[k] if timed_dom else None)
             return
-        path.plan_ahead(dtabs[k0 % n_distinct], k0 % 2, after=start_ev)
+        R = path.RING
+        path.plan_ahead(dtabs[k0 % n_distinct], k0 % R, after=start_ev)
         for k in range(n):
             kk = k0 + k
             if k + 1 < n:
-                path.plan_ahead(dtabs[(kk + 1) % n_distinct], (kk + 1) % 2)
-            stream.wait_event(path._ready[kk % 2])
-            p = path._ring[kk % 2]
+                path.plan_ahead(dtabs[(kk + 1) % n_distinct], (kk + 1) % R)
+            stream.wait_event(path._ready[kk % R])
+            p = path._ring[kk % R]
             path.dispatch(p, arenas[kk % n_distinct], stream)
             if timed_dom:
                 timed_dom[k][0].record(stream)
-            path.return_scatter(p, stream)
+            ev = path.return_scatter(p, stream)
             if timed_dom:
                 timed_dom[k][1].record(stream)
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            path._freed[kk % 2] = ev
+            path._freed[kk % R] = ev
 
     graphs = None
     if args.graphs and args.pipeline:
@@ -322,6 +321,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0.record(stream)
         run_steps(args.warmup, args.steps, ev_dom, start_ev=t0)
+        path.finish(stream)
         t1.record(stream)
         torch.cuda.synchronize()
     path.check_wait()

@@ -167,6 +167,15 @@ int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                        uint64_t* const* flags_peers, uint32_t* sync, uint64_t* epoch_ctr,
                        void* stream);
 
+/* General form: segments whose destination rank is `skip_rank` are not
+ * copied (-1: copy all); flags_peers may be NULL (no completion signal).
+ * grid_ctas < 0 launches -grid_ctas CTAs without shared memory, so the copy
+ * can co-reside with a kernel that holds the SMs' shared memory. */
+int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t which,
+                   void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
+                   int32_t skip_rank, uint64_t* const* flags_peers, uint32_t* sync,
+                   uint64_t* epoch_ctr, void* stream);
+
 /* One contiguous 8-byte-aligned byte range with the same copy engine as
  * mux_segcopy (local or NVLink-peer dst/src); used by the NVLink probe. */
 int mux_copy_bytes(void* dst, const void* src, int64_t n, int32_t grid_ctas, void* stream);
@@ -195,6 +204,12 @@ int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, const int64_t
  * destination table: row_dst[src_row] = (dst_rank << 40) | dst_row. */
 int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_t group,
                     int64_t* row_dst, int64_t n_rows, void* stream);
+
+/* As mux_return_rows; with stage_slot >= 0 the pieces addressed to other
+ * ranks map to (stage_slot << 40) | source row instead, so a projector GEMM
+ * can store them locally (out_bases[stage_slot]) for a later push. */
+int mux_return_rows_ex(const mux_plan_cfg* cfg, const void* plan, int32_t group,
+                       int64_t* row_dst, int64_t n_rows, int32_t stage_slot, void* stream);
 
 /* MUX_RET_STAGED: per-row destination of the owner's staging rows of
  * `group`: row_dst[stage_off + t] = (me << 40) | (llm_row + t).  lens: the

@@ -123,6 +123,7 @@ struct SegArgs {
   uint64_t* const* flags_peers;
   uint64_t* epoch_ctr;  // device counter: epoch = ++*epoch_ctr (graph-replay safe)
   int32_t me, world;
+  int32_t skip_rank;    // segments addressed to this rank are not copied (-1: none)
 };
 
 // Work distribution is dynamic: CTAs grab kGrab chunks at a time from a
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int sm
     int64_t next = c0(s + 1);
     for (int64_t c = c_begin; c < c_end; ++c) {
       while (c >= next) next = c0(++s + 1);
+      if (a.rank[s] == a.skip_rank) continue;
       const int g = a.group[s];
       const int64_t rb = a.row_bytes[g];
       const int64_t lo_b = (c - c0(s)) * a.chunk_bytes;
@@ -282,14 +284,20 @@ __global__ void __launch_bounds__(256) standin_kernel(Plan p, int S, int me, int
   }
 }
 
-__global__ void return_rows_kernel(Plan p, int group, int64_t* row_dst, int64_t n_rows) {
+// row_dst[src row] = (dst rank << 40) | dst row of every return piece of
+// `group`; with stage_slot >= 0, pieces for other ranks go to slot
+// `stage_slot` at their own (encoder-order) row instead, for a later push.
+__global__ void return_rows_kernel(Plan p, int group, int64_t* row_dst, int64_t n_rows, int me,
+                                   int stage_slot) {
   const int64_t npieces = p.hdr[MUX_H_N_RETURN];
   for (int64_t s = blockIdx.x; s < npieces; s += gridDim.x) {
     if (p.rgroup[s] != group) continue;
     const int64_t src = p.rsrc[s], dst = p.rdst[s], n = p.rrows[s];
-    const int64_t tag = (int64_t)p.rrank[s] << 40;
+    const bool staged = stage_slot >= 0 && p.rrank[s] != me;
+    const int64_t tag = (int64_t)(staged ? stage_slot : p.rrank[s]) << 40;
+    const int64_t base = staged ? src : dst;
     for (int64_t t = threadIdx.x; t < n; t += blockDim.x)
-      if (src + t < n_rows) row_dst[src + t] = tag | (dst + t);
+      if (src + t < n_rows) row_dst[src + t] = tag | (base + t);
   }
 }
 
@@ -331,6 +339,14 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
                                   void* const* src_bases, void* const* dst_bases,
                                   int32_t grid_ctas, uint64_t* const* flags_peers,
                                   uint32_t* sync, uint64_t* epoch_ctr, void* stream) {
+  return mux_segcopy_ex(cfg, plan, which, src_bases, dst_bases, grid_ctas, -1, flags_peers, sync,
+                        epoch_ctr, stream);
+}
+
+extern "C" int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t which,
+                              void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
+                              int32_t skip_rank, uint64_t* const* flags_peers, uint32_t* sync,
+                              uint64_t* epoch_ctr, void* stream) {
   mux_plan_layout L;
   int st = mux_plan_layout_of(cfg, &L);
   if (st) return st;
@@ -356,14 +372,19 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
   a.epoch_ctr = epoch_ctr;
   a.me = cfg->me;
   a.world = cfg->world;
+  a.skip_rank = skip_rank;
   if (!sync || (flags_peers && !epoch_ctr)) {
     set_error("segment copy needs its sync counters (and an epoch counter to signal)");
     return MUX_ERR_VALUE;
   }
-  const int grid = grid_ctas > 0 ? grid_ctas : num_sms() * 8;
-  // stage the chunk prefix in shared memory when the segment bound is small
+  // grid_ctas < 0: "co-resident" launch of -grid_ctas CTAs with no shared
+  // memory, so the copy can run beside a kernel that holds the SMs' shared
+  // memory (the projector GEMM); otherwise the chunk prefix is staged in
+  // shared memory when the segment bound is small.
+  const bool lean = grid_ctas < 0;
+  const int grid = lean ? -grid_ctas : (grid_ctas > 0 ? grid_ctas : num_sms() * 8);
   const int max_segs = ret ? cfg->S * (cfg->sp + 1) + 1 : cfg->S + 1;
-  const int smem_segs = max_segs + 1 <= 4096 ? max_segs + 1 : 0;
+  const int smem_segs = !lean && max_segs + 1 <= 4096 ? max_segs + 1 : 0;
   segcopy_kernel<<<grid, kCopyThreads, smem_segs * sizeof(int32_t),
                    static_cast<cudaStream_t>(stream)>>>(a, smem_segs);
   MUX_CUDA(cudaGetLastError());
@@ -407,11 +428,18 @@ extern "C" int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, co
 
 extern "C" int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_t group,
                                int64_t* row_dst, int64_t n_rows, void* stream) {
+  return mux_return_rows_ex(cfg, plan, group, row_dst, n_rows, -1, stream);
+}
+
+extern "C" int mux_return_rows_ex(const mux_plan_cfg* cfg, const void* plan, int32_t group,
+                                  int64_t* row_dst, int64_t n_rows, int32_t stage_slot,
+                                  void* stream) {
   mux_plan_layout L;
   int st = mux_plan_layout_of(cfg, &L);
   if (st) return st;
   Plan p = make_plan_const(plan, L);
-  return_rows_kernel<<<256, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, group, row_dst, n_rows);
+  return_rows_kernel<<<256, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, group, row_dst, n_rows,
+                                                                         cfg->me, stage_slot);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

@@ -10,8 +10,8 @@ plan is integer-only and bit-identical on every rank), then *pushes* its rows:
                     placeholder positions (SPEC.md:408-416 restore_order and
                     SPEC.md:462-470 plan_reshard, one hop instead of the
                     paper's send-then-reshard)
-  projector         with a projector, the return is the tcgen05 GEMM whose
-                    epilogue stores each output row at its (rank, row).
+  projector         with a projector, the tcgen05 GEMM whose epilogue stores each
+                    output row at its (rank, row); across GPUs see `MuxPath`.
 
 Receive windows, LLM buffers and completion flags are torch symmetric-memory
 allocations (CUDA VMM + IPC under the hood); the kernels get raw peer pointers.
@@ -54,6 +54,10 @@ def _ptr_table(ptrs, device) -> torch.Tensor:
     return torch.tensor([int(p) for p in ptrs], dtype=torch.int64, device=device)
 
 
+def _event(timing: bool = False) -> torch.cuda.Event:
+    return torch.cuda.Event(enable_timing=timing)
+
+
 class MuxPath:
     """Per-rank data path for one workload shape.
 
@@ -63,6 +67,19 @@ class MuxPath:
     d_enc[g] the encoder hidden, d_llm the LLM hidden.  projector=False
     returns d_llm-wide encoder rows bit-exactly; projector=True returns
     Y = X W_g^T (+ b_g) from d_enc-wide rows.
+
+    Projector across GPUs (projector_return, env MUX_PROJECTOR_RETURN):
+      "fused" (default)  the GEMM runs on the encoder rank (where LPT balanced
+          the rows) and its epilogue stores every output row straight into the
+          owner's packed buffer over NVLink: compute and collective in one kernel;
+      "staged"  the narrow d_enc rows are pushed to the LLM owner's
+          staging window (3.2x fewer NVLink bytes than d_llm rows) and the
+          owner projects them on a projector stream, overlapped with the next
+          step's dispatch and return (staging and LLM buffers alternate, so
+          step k's LLM rows are final once the event `return_scatter` returns
+          has fired and stay valid until step k+2's projector runs); the
+          owners' rows are not balanced by the encoder-side LPT, so at 2 GPUs it
+          measured no faster than "fused".
     """
 
     def __init__(self, *, capacity: int, gbs: int, dp: int, sp: int = 1, world: int = 1,
@@ -74,31 +91,25 @@ class MuxPath:
         self.world, self.rank, self.method, self.pooled = world, rank, method, pooled
         self.d_in, self.d_enc, self.d_llm = tuple(d_in), tuple(d_enc), d_llm
         self.projector = projector
-        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.device = dev = device or torch.device("cuda", torch.cuda.current_device())
         self.group = group
         self.timeout_ms = wait_timeout_ms
         self.d_ret = tuple(d_enc) if projector else (d_llm, d_llm)
-        # projector across GPUs, two designs:
-        #  "fused"  (default) the GEMM runs on the encoder rank (where LPT balanced
-        #           the rows) and its epilogue bulk-stores each output row straight
-        #           into the owner's packed buffer over NVLink;
-        #  "staged" the narrow d_enc rows go to the owner's staging window (3.2x
-        #           fewer NVLink bytes), which then projects locally (its rows are
-        #           not balanced by the encoder-side LPT).
         mode = projector_return or os.environ.get("MUX_PROJECTOR_RETURN", "fused")
         if mode not in ("fused", "staged"):
             raise ValueError(f"projector_return must be 'fused' or 'staged', not {mode!r}")
         self.projector_return = mode
-        self.ret_mode = _lib.RET_STAGED if projector and world > 1 and mode == "staged" \
-            else _lib.RET_FINAL
+        self.staged = bool(projector and world > 1 and mode == "staged")
+        self.ret_mode = _lib.RET_STAGED if self.staged else _lib.RET_FINAL
         rows = max_rows or gbs * capacity                       # all batch tokens
         llm_rows = (gbs // dp) * capacity // sp + gbs // dp + 1  # one rank's shards
         self.max_rows, self.max_llm_rows = rows, llm_rows
-        dev = self.device
+        self.num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.gemm_ctas = 0  # 0: one CTA per SM; plan_ahead() leaves one SM to the planner
+
         self.recv = [_Window(rows * d_in[g] * 2, dev, group, world) for g in range(N_GROUPS)]
-        self.llm = _Window(llm_rows * d_llm * 2, dev, group, world)
-        self.stage = [_Window(llm_rows * d_enc[g] * 2, dev, group, world) for g in range(N_GROUPS)] \
-            if self.ret_mode == _lib.RET_STAGED else None
+        n_llm = 2 if self.staged else 1
+        self.llm_bufs = [_Window(llm_rows * d_llm * 2, dev, group, world) for _ in range(n_llm)]
         self.flags = _Window(8 * world, dev, group, world)
         self.flags.tensor.zero_()
         self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
@@ -106,26 +117,32 @@ class MuxPath:
         self.sync = torch.zeros(4, dtype=torch.int32, device=dev)  # copy counters x2
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
-        # pointer tables for the copy kernels
         self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
                                     for g in range(N_GROUPS)], dev)
-        self.llm_dst = _ptr_table(self.llm.ptrs, dev)
-        if self.stage is not None:
-            self.stage_dst = _ptr_table([self.stage[g].ptrs[r] for r in range(world)
-                                         for g in range(N_GROUPS)], dev)
+        self.llm_dst = [_ptr_table(b.ptrs, dev) for b in self.llm_bufs]
         self.enc_src = _ptr_table([t.data_ptr() for t in self.enc_out], dev)
-        self.num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        self.gemm_ctas = 0  # 0: one CTA per SM; plan_ahead() leaves one SM to the planner
         self.flag_ptrs = _ptr_table(self.flags.ptrs, dev)
         self._arena_tables: dict = {}
         self._plan: Plan | None = None
+        self._ring = None
+        self.last_llm = 0
+        if self.staged:
+            self.stage = [[_Window(llm_rows * d_enc[g] * 2, dev, group, world)
+                           for g in range(N_GROUPS)] for _ in range(2)]
+            self.stage_dst = [_ptr_table([self.stage[b][g].ptrs[r] for r in range(world)
+                                          for g in range(N_GROUPS)], dev) for b in range(2)]
+            self._proj = torch.cuda.Stream(dev)
+            self._ev_p = [None, None]
+            self._kret = 0
+            self.row_dst_b = [torch.empty(llm_rows, dtype=torch.int64, device=dev)
+                              for _ in range(2)]
         if world > 1:
             torch.cuda.synchronize()
             self.flags.handle.barrier()
         if projector:
             self.weight = [None] * N_GROUPS
             self.bias = [None] * N_GROUPS
-            self.row_dst = torch.empty(max(rows, llm_rows), dtype=torch.int64, device=dev)
+            self.row_dst = torch.empty(rows, dtype=torch.int64, device=dev)
 
     # ------------------------------------------------------------------ setup
     def set_projector(self, group: int, weight: torch.Tensor, bias: torch.Tensor | None = None):
@@ -141,9 +158,18 @@ class MuxPath:
                         row_bytes_in=tuple(2 * d for d in self.d_in),
                         row_bytes_ret=tuple(2 * d for d in self.d_ret), ret_mode=self.ret_mode)
 
+    @property
+    def llm(self) -> _Window:
+        return self.llm_bufs[self.last_llm]
+
     def llm_view(self, rows: int | None = None) -> torch.Tensor:
+        """Packed LLM input of this rank (with alternating buffers: the latest step's)."""
         n = self.max_llm_rows if rows is None else rows
         return self.llm.tensor[: n * self.d_llm * 2].view(torch.bfloat16).view(n, self.d_llm)
+
+    def zero_llm(self):
+        for b in self.llm_bufs:
+            b.tensor.zero_()
 
     def recv_view(self, group: int, rows: int) -> torch.Tensor:
         d = self.d_in[group]
@@ -155,22 +181,27 @@ class MuxPath:
 
     # ------------------------------------------------------------------ stages
     def plan(self, dtab: DeviceTable, stream=None) -> Plan:
+        """In-line plan into the single plan buffer (see plan_ahead for the ring)."""
+        self.finish(stream)  # an overlapped projector may still read the buffer
         cfg = self.cfg_for(dtab.table)
         self._plan = plan_step(dtab, cfg, self._plan, stream)
         return self._plan
 
-    # ------------------------------------------------------- planner pipelining
     # The plan of step k+1 needs only metadata, so it runs on a high-priority
-    # side stream while step k's rows move; two plan buffers alternate.
+    # side stream while step k's rows move.  RING plan buffers rotate: a plan
+    # is read until its step's (possibly overlapped) projector finishes, so
+    # with an overlapped projector two buffers would stall the planner.
+    RING = 4
+
     def _ensure_ring(self):
-        if getattr(self, "_ring", None) is None:
+        if self._ring is None:
             self._side = torch.cuda.Stream(self.device, priority=-1)
-            self._ring = [None, None]
-            self._ready = [torch.cuda.Event(), torch.cuda.Event()]
-            self._freed = [None, None]
+            self._ring = [None] * self.RING
+            self._ready = [_event() for _ in range(self.RING)]
+            self._freed = [None] * self.RING
 
     def plan_ahead(self, dtab: DeviceTable, slot: int, after=None) -> Plan:
-        """Plan `dtab` into ring slot 0/1 on the side stream.  `after`: an
+        """Plan `dtab` into ring slot `slot` (0..RING-1) on the side stream.  `after`: an
         event the plan must follow (e.g. the step-table upload)."""
         self._ensure_ring()
         self.gemm_ctas = self.num_sms - 1
@@ -184,16 +215,13 @@ class MuxPath:
         self._ready[slot].record(side)
         return self._ring[slot]
 
-    def run_planned(self, slot: int, arenas, stream=None):
+    def run_planned(self, slot: int, arenas, stream=None) -> Plan:
         """Dispatch + return of the plan in ring `slot` on the main stream."""
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         main.wait_event(self._ready[slot])
         p = self._ring[slot]
         self.dispatch(p, arenas, main)
-        self.return_scatter(p, main)
-        ev = torch.cuda.Event()
-        ev.record(main)
-        self._freed[slot] = ev
+        self._freed[slot] = self.return_scatter(p, main)
         return p
 
     def _arena_table(self, arenas) -> torch.Tensor:
@@ -207,6 +235,8 @@ class MuxPath:
         return t
 
     def _exchange(self, plan: Plan, which: int, src, dst, stream):
+        """One segment-copy exchange; across GPUs the last CTA signals every
+        peer and a flag wait orders the stream after every peer's copy."""
         L = _lib.lib()
         s = _stream_ptr(stream)
         if self.world == 1:
@@ -214,10 +244,12 @@ class MuxPath:
                                      dst.data_ptr(), 0, self.sync[2 * which:].data_ptr(), s),
                        "mux_segcopy")
             return
-        _lib.check(L.mux_segcopy_signal(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
-                                        dst.data_ptr(), 0, self.flag_ptrs.data_ptr(),
-                                        self.sync[2 * which:].data_ptr(), self.epoch_ctr.data_ptr(),
-                                        s), "mux_segcopy_signal")
+        # beside an overlapped projector (which holds shared memory) copy CTAs stay lean
+        grid = -2 * self.num_sms if self.staged else 0
+        _lib.check(L.mux_segcopy_ex(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
+                                    dst.data_ptr(), grid, -1, self.flag_ptrs.data_ptr(),
+                                    self.sync[2 * which:].data_ptr(), self.epoch_ctr.data_ptr(),
+                                    s), "mux_segcopy_ex")
         _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch_ctr.data_ptr(),
                               self.timeout_ms, self.wait_err.data_ptr(), s), "mux_wait")
 
@@ -233,52 +265,89 @@ class MuxPath:
                                              self.d_ret[g], self.enc_out[g].data_ptr(),
                                              _stream_ptr(stream)), "mux_encoder_standin")
 
-    def return_scatter(self, plan: Plan, stream=None):
-        """Return + scatter (projector off) or projector GEMM + scatter (on).
+    def return_scatter(self, plan: Plan, stream=None) -> torch.cuda.Event:
+        """Return + scatter (projector off) or projector + scatter (on).
 
-        No host synchronisation: row counts are read from the plan header on
-        the device (mux_proj_scatter_dev)."""
+        Returns the event after which `plan` is no longer read and this step's
+        LLM rows are final.  No host synchronisation: row counts come from the
+        plan header on the device."""
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
         if not self.projector:
-            self._exchange(plan, 1, self.enc_src, self.llm_dst, stream)
-            return
+            self._exchange(plan, 1, self.enc_src, self.llm_dst[0], main)
+        elif self.staged:
+            return self._return_staged(plan, main)
+        else:
+            self._project(plan, main)
+        ev = _event()
+        ev.record(main)
+        return ev
+
+    def _project(self, plan: Plan, main):
+        """GEMM on this (encoder) rank; the epilogue stores every row at its
+        (rank, row), on this GPU or an NVLink peer."""
         L = _lib.lib()
-        s = _stream_ptr(stream)
+        s = _stream_ptr(main)
         hdr = plan.ptr + plan.layout.header
-        if self.ret_mode == _lib.RET_STAGED:
-            # d_enc rows -> owner's staging window (NVLink push + flags), then local GEMM
-            self._exchange(plan, 1, self.enc_src, self.stage_dst, stream)
-            for g in range(N_GROUPS):
-                if self.weight[g] is None:
-                    continue
-                _lib.check(L.mux_stage_rows(C.byref(plan.cfg), plan.ptr, plan.lens_ptr, g,
-                                            self.row_dst.data_ptr(), self.max_llm_rows, s),
-                           "mux_stage_rows")
-                b = self.bias[g]
-                _lib.check(L.mux_proj_scatter_dev(
-                    self.stage[g].tensor.data_ptr(), self.weight[g].data_ptr(),
-                    0 if b is None else b.data_ptr(), self.max_llm_rows,
-                    hdr + 8 * (_lib.H_STAGE_ROWS0 + g), self.d_enc[g], self.d_llm,
-                    self.row_dst.data_ptr(), self.llm_dst.data_ptr(), self.gemm_ctas, s),
-                    "mux_proj_scatter_dev")
-            return
         for g in range(N_GROUPS):
             if self.weight[g] is None:
                 continue
-            m_dev = hdr + 8 * (_lib.H_RECV_ROWS0 + g)
             _lib.check(L.mux_return_rows(C.byref(plan.cfg), plan.ptr, g, self.row_dst.data_ptr(),
                                          self.max_rows, s), "mux_return_rows")
             b = self.bias[g]
-            _lib.check(L.mux_proj_scatter_dev(self.enc_out[g].data_ptr(), self.weight[g].data_ptr(),
-                                              0 if b is None else b.data_ptr(), self.max_rows,
-                                              m_dev, self.d_enc[g], self.d_llm,
-                                              self.row_dst.data_ptr(), self.llm_dst.data_ptr(),
-                                              self.gemm_ctas, s), "mux_proj_scatter_dev")
-        if self.world > 1:  # (direct mode across GPUs: GEMM stored to peers)
+            _lib.check(L.mux_proj_scatter_dev(
+                self.enc_out[g].data_ptr(), self.weight[g].data_ptr(),
+                0 if b is None else b.data_ptr(), self.max_rows,
+                hdr + 8 * (_lib.H_RECV_ROWS0 + g), self.d_enc[g], self.d_llm,
+                self.row_dst.data_ptr(), self.llm_dst[0].data_ptr(), self.gemm_ctas, s),
+                "mux_proj_scatter_dev")
+        if self.world > 1:
             _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(),
                                     self.epoch_ctr.data_ptr(), s), "mux_signal")
             _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(),
                                   self.epoch_ctr.data_ptr(), self.timeout_ms,
                                   self.wait_err.data_ptr(), s), "mux_wait")
+
+    def _return_staged(self, plan: Plan, main) -> torch.cuda.Event:
+        """d_enc rows -> the owner's staging window (main-stream exchange), then
+        the owner's GEMM on the projector stream, overlapped with what follows."""
+        L = _lib.lib()
+        b = self._kret % 2
+        self._kret += 1
+        if self._ev_p[b] is not None:  # the projector of step k-2 has read stage[b]
+            main.wait_event(self._ev_p[b])
+        self._exchange(plan, 1, self.enc_src, self.stage_dst[b], main)
+        ev_r = _event()
+        ev_r.record(main)
+        proj = self._proj
+        proj.wait_event(ev_r)
+        s = _stream_ptr(proj)
+        hdr = plan.ptr + plan.layout.header
+        rd = self.row_dst_b[b]
+        for g in range(N_GROUPS):
+            if self.weight[g] is None:
+                continue
+            _lib.check(L.mux_stage_rows(C.byref(plan.cfg), plan.ptr, plan.lens_ptr, g,
+                                        rd.data_ptr(), self.max_llm_rows, s), "mux_stage_rows")
+            bias = self.bias[g]
+            _lib.check(L.mux_proj_scatter_dev(
+                self.stage[b][g].tensor.data_ptr(), self.weight[g].data_ptr(),
+                0 if bias is None else bias.data_ptr(), self.max_llm_rows,
+                hdr + 8 * (_lib.H_STAGE_ROWS0 + g), self.d_enc[g], self.d_llm,
+                rd.data_ptr(), self.llm_dst[b].data_ptr(), self.gemm_ctas, s),
+                "mux_proj_scatter_dev")
+        ev_p = _event(timing=True)
+        ev_p.record(proj)
+        self._ev_p[b] = ev_p
+        self.last_llm = b
+        return ev_p
+
+    def finish(self, stream=None):
+        """Make `stream` wait for every outstanding overlapped projector."""
+        if self.staged:
+            main = stream if stream is not None else torch.cuda.current_stream(self.device)
+            for ev in self._ev_p:
+                if ev is not None:
+                    main.wait_event(ev)
 
     # ------------------------------------------------------------ CUDA graphs
     def capture_steps(self, dtabs, arenas_list):
@@ -328,6 +397,7 @@ class StepGraphs:
                 plan_step(dtabs[j], cfgs[j], plans[j], side)
                 path.dispatch(plans[i], arenas_list[i], main)
                 path.return_scatter(plans[i], main)
+                path.finish(main)
                 main.wait_stream(side)
             self.graphs.append(g)
         self.dtabs, self.cfgs = dtabs, cfgs

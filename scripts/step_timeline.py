@@ -81,11 +81,11 @@ def main():
         if not proj:
             if world == 1:
                 L.mux_segcopy(C.byref(p.cfg), p.ptr, 1, path.enc_src.data_ptr(),
-                              path.llm_dst.data_ptr(), 0, path.sync[2:].data_ptr(), s)
+                              path.llm_dst[0].data_ptr(), 0, path.sync[2:].data_ptr(), s)
                 marks.append(("return copy", ev()))
             else:
                 L.mux_segcopy_signal(C.byref(p.cfg), p.ptr, 1, path.enc_src.data_ptr(),
-                                     path.llm_dst.data_ptr(), 0, path.flag_ptrs.data_ptr(),
+                                     path.llm_dst[0].data_ptr(), 0, path.flag_ptrs.data_ptr(),
                                      path.sync[2:].data_ptr(), path.epoch_ctr.data_ptr(), s)
                 marks.append(("return copy", ev()))
                 L.mux_wait(world, path.flags.tensor.data_ptr(), path.epoch_ctr.data_ptr(), 20000,
@@ -96,7 +96,7 @@ def main():
             marks.append(("return_rows + projector GEMM (+signal/wait)", ev()))
         else:
             L.mux_segcopy_signal(C.byref(p.cfg), p.ptr, 1, path.enc_src.data_ptr(),
-                                 path.stage_dst.data_ptr(), 0, path.flag_ptrs.data_ptr(),
+                                 path.stage_dst[0].data_ptr(), 0, path.flag_ptrs.data_ptr(),
                                  path.sync[2:].data_ptr(), path.epoch_ctr.data_ptr(), s)
             marks.append(("return copy (d_enc rows)", ev()))
             L.mux_wait(world, path.flags.tensor.data_ptr(), path.epoch_ctr.data_ptr(), 20000,
@@ -107,11 +107,11 @@ def main():
                 L.mux_stage_rows(C.byref(p.cfg), p.ptr, p.lens_ptr, g, path.row_dst.data_ptr(),
                                  path.max_llm_rows, s)
                 marks.append((f"stage_rows g{g}", ev()))
-                L.mux_proj_scatter_dev(path.stage[g].tensor.data_ptr(),
+                L.mux_proj_scatter_dev(path.stage[0][g].tensor.data_ptr(),
                                        path.weight[g].data_ptr(), 0, path.max_llm_rows,
                                        hdr + 8 * (_lib.H_STAGE_ROWS0 + g), path.d_enc[g],
                                        path.d_llm, path.row_dst.data_ptr(),
-                                       path.llm_dst.data_ptr(), 0, s)
+                                       path.llm_dst[0].data_ptr(), 0, s)
                 marks.append((f"GEMM g{g}", ev()))
         torch.cuda.synchronize()
         if k >= 3:

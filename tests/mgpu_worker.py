@@ -54,7 +54,8 @@ def main():
         gbs = cfg["gbs_per_replica"] * dp
     path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
                    d_in=d_in, d_enc=d_enc, d_llm=d_llm, device=dev, group=dist.group.WORLD,
-                   projector=proj, projector_return="staged" if "staged" in sys.argv else "fused")
+                   projector=proj,
+                   projector_return="staged" if "staged" in sys.argv else "fused")
     if proj:
         gw = torch.Generator().manual_seed(9)
         Ws = [(torch.randn(d_llm, d_enc[g], generator=gw) / d_enc[g] ** 0.5).to(torch.bfloat16)
@@ -82,12 +83,13 @@ def main():
             dtab = planner.DeviceTable(table, dev)
             plan = path.plan(dtab)
             plan.check(table)
-            path.llm_view().zero_()
+            path.zero_llm()
             torch.cuda.synchronize()
             dist.barrier()
             path.dispatch(plan, [a.to(dev) for a in arenas[rank]])
             path.encode_standin(plan, dtab)
             path.return_scatter(plan)
+            path.finish()
             torch.cuda.synchronize()
             path.check_wait()
             ar = [[a.view(torch.int16).numpy().view(np.uint16) for a in arenas[r]]
