@@ -415,7 +415,7 @@ def run_ours(args):
     if rank == 0:
         line["clocks"] = clk.summary()
         if world == 1:
-            line["cpu_baseline"] = cpu_baseline(name, tables[0], projector, quick=True)
+            line["cpu_baseline"] = cpu_baseline(name, tables[0], projector, world)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -528,83 +528,97 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
 # CPU reference arm (oracle port; the reference itself never moves token data)
 # ----------------------------------------------------------------------------
 
-def cpu_baseline(name, table, projector, quick=False, budget_s=None):
-    """Time the CPU port (oracle planner + torch-CPU data plane) on one step.
+def cpu_baseline(name, table, projector, world=1):
+    """Time the CPU port on one step of the workload at `world` GPUs' scale.
 
-    Bounded sample: one step of the workload (full token counts); the
-    projector GEMM, when on, is timed on a 4096-row slice and scaled.
+    Code timed: the oracle planner (FFD + batch + LPT + reshard; restates the
+    reference's hybrid_pack / build_global_batch, workload.py:240-278) and the
+    data plane in torch-CPU over all ranks' rows at once (index_select pack,
+    index_copy_ return/scatter; the projector as an fp32 matmul timed on a
+    4096-row slice and extrapolated).  All host threads.  One step = the bounded
+    sample.
     """
     import torch
 
     from oracle import planner as oplan
     from paper_2605_08962_b200 import configs
 
-    cfg = configs.CONFIGS[name]
+    cfg, dp, sp, gbs = workload(name, world)
     threads = len(os.sched_getaffinity(0))
     torch.set_num_threads(threads)
     t = dict(lens=table.lens.astype(np.int64), mods=table.mods.astype(np.int64), ids=table.ids,
              carry_seq=table.carry_seq.astype(np.int64), n_carry_seqs=table.n_carry_seqs,
              chunk_off=table.chunk_off.tolist())
-    gbs = cfg["gbs_per_replica"]
     d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, configs.D_LLM
     t0 = time.perf_counter()
-    o = oplan.plan_step(t, configs.CAPACITY, gbs, 1, 1, 1)
+    o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world)
     t_plan = time.perf_counter() - t0
-    rows = [int(o["arena_rows"][0, g]) for g in range(2)]
+    lens = t["lens"]
+    items = np.flatnonzero(o["enc"] >= 0)
+    rows = [int(o["arena_rows"][:, g].sum()) for g in range(2)]
+    # all ranks' arenas / receive buffers / LLM buffers stacked: one global row space
+    a_base = np.zeros((world, 2), np.int64)
+    r_base = np.zeros((world, 2), np.int64)
+    for g in range(2):
+        a_base[1:, g] = np.cumsum(o["arena_rows"][:-1, g])
+        r_base[1:, g] = np.cumsum(o["recv_rows"][:-1, g])
+    l_base = np.zeros(world, np.int64)
+    l_base[1:] = np.cumsum(o["llm_rows"][:-1])
     arenas = [torch.randn(max(r, 1), d_in[g]).to(torch.bfloat16) for g, r in enumerate(rows)]
     recv = [torch.empty(max(r, 1), d_in[g], dtype=torch.bfloat16) for g, r in enumerate(rows)]
     d_ret = d_enc if projector else (d_llm, d_llm)
     enc = [torch.randn(max(r, 1), d_ret[g]).to(torch.bfloat16) for g, r in enumerate(rows)]
-    llm = torch.zeros(int(o["llm_rows"][0]), d_llm, dtype=torch.bfloat16)
-    lens = t["lens"]
-    items = np.flatnonzero(o["enc"] >= 0)
-    # pack: index gather per group
+    llm = torch.zeros(int(o["llm_rows"].sum()), d_llm, dtype=torch.bfloat16)
     t0 = time.perf_counter()
-    for g in range(2):
+    for g in range(2):  # pack + dispatch: origin arena rows -> encoder receive rows
         src, dst = [], []
         for i in items:
             if o["group"][i] == g:
                 L = int(lens[i])
-                src.append(np.arange(o["arena_off"][i], o["arena_off"][i] + L))
-                dst.append(np.arange(o["enc_off"][i], o["enc_off"][i] + L))
+                a = a_base[o["origin"][i], g] + o["arena_off"][i]
+                r = r_base[o["enc"][i], g] + o["enc_off"][i]
+                src.append(np.arange(a, a + L))
+                dst.append(np.arange(r, r + L))
         if src:
-            s, d = torch.from_numpy(np.concatenate(src)), torch.from_numpy(np.concatenate(dst))
-            recv[g].index_copy_(0, d, arenas[g].index_select(0, s))
+            sI, dI = torch.from_numpy(np.concatenate(src)), torch.from_numpy(np.concatenate(dst))
+            recv[g].index_copy_(0, dI, arenas[g].index_select(0, sI))
     t_pack = time.perf_counter() - t0
-    # return + scatter (+ projector)
     t0 = time.perf_counter()
+    extra = 0.0
     scale = 1.0
-    for g in range(2):
+    for g in range(2):  # return (+ projector) + scatter into the packed LLM rows
         src, dst = [], []
-        for (i, sr, _, dr, n) in o["pieces"]:
+        for (i, sr, dr_rank, dr, n) in o["pieces"]:
             if o["group"][i] == g:
-                src.append(np.arange(sr, sr + n))
-                dst.append(np.arange(dr, dr + n))
+                e = r_base[o["enc"][i], g]
+                src.append(np.arange(e + sr, e + sr + n))
+                dst.append(np.arange(l_base[dr_rank] + dr, l_base[dr_rank] + dr + n))
         if not src:
             continue
-        s, d = torch.from_numpy(np.concatenate(src)), torch.from_numpy(np.concatenate(dst))
-        x = enc[g].index_select(0, s)
+        sI, dI = torch.from_numpy(np.concatenate(src)), torch.from_numpy(np.concatenate(dst))
+        x = enc[g].index_select(0, sI)
         if projector:
             W = torch.randn(d_llm, d_enc[g]).to(torch.bfloat16)
             m = min(4096, x.shape[0])
             tg = time.perf_counter()
             y = (x[:m].float() @ W.float().t()).to(torch.bfloat16)
             tm = time.perf_counter() - tg
-            scale_t = tm * (x.shape[0] / m - 1)   # remaining rows, extrapolated
-            t0 -= scale_t
-            x = torch.cat([y, torch.zeros(x.shape[0] - m, d_llm, dtype=torch.bfloat16)])
             scale = x.shape[0] / m
-        llm.index_copy_(0, d, x)
-    t_ret = time.perf_counter() - t0
+            extra += tm * (scale - 1)  # the remaining rows, extrapolated
+            x = torch.cat([y, torch.zeros(x.shape[0] - m, d_llm, dtype=torch.bfloat16)])
+        llm.index_copy_(0, dI, x)
+    t_ret = time.perf_counter() - t0 + extra
     M = int(o["recv_rows"].sum())
     total = t_plan + t_pack + t_ret
-    sample = (f"one {name} step: {M} modality tokens, oracle planner + torch-CPU gather/scatter"
-              + (f"; projector timed on 4096 rows, scaled x{scale:.1f}" if projector else ""))
+    sample = (f"one {name} step at {world} GPU(s) simulated in-process: {M} modality tokens; "
+              "oracle planner + torch-CPU gather/scatter"
+              + (f"; projector timed on 4096 rows, x{scale:.1f} extrapolated" if projector else ""))
     return {"value": M / total, "unit": "tokens/s", "cores": threads, "kind": "port",
             "sample": sample, "seconds": {"plan": t_plan, "pack": t_pack, "return": t_ret}}
 
 
 def run_reference(args):
+    """CPU reference arm: rank 0 only; the other ranks exit without work."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -615,7 +629,7 @@ def run_reference(args):
     tables = generate_steps_host(name, world, max(1, min(args.steps + args.warmup, 4)))
     vals = []
     for k in range(args.warmup + args.steps):
-        r = cpu_baseline_world(name, tables[k % len(tables)], world, cfg["projector"])
+        r = cpu_baseline(name, tables[k % len(tables)], bool(cfg["projector"]), world)
         if k >= args.warmup:
             vals.append(r)
     v = float(np.mean([r["value"] for r in vals]))
@@ -647,21 +661,14 @@ def generate_steps_host(name, world, n_steps):
         b, rest, drawn, chunks = owork.generate(descs, cfg["phases"], False, step, cfg["seed"],
                                                 gbs, dp, 1, configs.CAPACITY,
                                                 carry if cfg["carry"] else None)
-        for s in drawn:
-            seen[s[0]] = s[1]
+        for smp in drawn:
+            seen[smp[0]] = smp[1]
         t = oplan.step_table(list(carry or []) if cfg["carry"] else [], drawn, chunks, seen)
         out.append(StepTable(t["lens"].astype(np.int32), t["mods"].astype(np.int32), t["ids"],
                              t["carry_seq"].astype(np.int32), t["n_carry_seqs"],
                              np.asarray(t["chunk_off"], np.int32)))
         carry = rest
     return out
-
-
-def cpu_baseline_world(name, table, world, projector):
-    if world == 1:
-        return cpu_baseline(name, table, projector)
-    # all ranks simulated in-process: the same gather/scatter over the whole batch
-    return cpu_baseline(name, table, projector)
 
 
 def main():
