@@ -70,6 +70,11 @@ extern "C" {
 #define MUX_H_RECV_ROWS1 13
 #define MUX_H_STAGE_ROWS0 14  /* rows staged on `me` for its projector, group 0/1 */
 #define MUX_H_STAGE_ROWS1 15
+#define MUX_H_N_GRAD 16      /* gradient-return pieces of rank `me` (LLM owner)  */
+#define MUX_H_GRAD_CHUNKS 17
+#define MUX_H_GRAD_BYTES 18
+#define MUX_H_GRAD_REMOTE 19
+#define MUX_H_STAMP0 20      /* 20..30: planner phase timestamps (globaltimer)  */
 #define MUX_H_SLOTS 32
 
 #define MUX_RET_FINAL 0  /* return rows go to their final packed-LLM rows           */
@@ -91,6 +96,7 @@ typedef struct {
   int32_t row_bytes_ret[MUX_N_GROUPS]; /* returned row bytes per group      */
   int32_t chunk_bytes;  /* copy work unit (0 = default 32 KiB)              */
   int32_t ret_mode;     /* MUX_RET_FINAL | MUX_RET_STAGED (sp == 1 only)      */
+  int32_t row_bytes_grad[MUX_N_GROUPS]; /* gradient-return row bytes (0: = ret) */
 } mux_plan_cfg;
 
 /* Byte offsets of every array inside the plan buffer (one device blob). */
@@ -117,6 +123,11 @@ typedef struct {
   int64_t rseg_src_row, rseg_dst_row, rseg_rows;    /* int64[S*(sp+1)]    */
   int64_t rseg_group, rseg_dst_rank;                /* int32[S*(sp+1)]    */
   int64_t rseg_chunk0;                              /* int64[S*(sp+1)+1]  */
+  /* gradient return (rank me as LLM owner): dY rows at my LLM rows back to
+   * their encoder rank's gradient buffer in encoder order     */
+  int64_t gseg_src_row, gseg_dst_row, gseg_rows;    /* int64[S*(sp+1)]    */
+  int64_t gseg_group, gseg_dst_rank;                /* int32[S*(sp+1)]    */
+  int64_t gseg_chunk0;                              /* int64[S*(sp+1)+1]  */
   int64_t total;
 } mux_plan_layout;
 
@@ -142,13 +153,17 @@ int mux_plan_check(const mux_plan_cfg* cfg, const int64_t* header_host,
                    const int64_t* ids_host, const int32_t* lens_host);
 
 /* Stand-alone partition of n weights over g ranks (kk_partition / LPT).
- * weights double[n], ids int64[n] (LPT tie-break), out int32[n].  Device
- * pointers; scratch int8[mux_assign_scratch_bytes(n, g)]. */
+ * weights double[n], ids int64[n] (LPT tie-break; NULL = index), out int32[n],
+ * init_loads double[g] (LPT only: loads the ranks start with, e.g. the
+ * residual capacity rule of CpHybrid; NULL = zeros).  Device
+ * pointers. */
 size_t mux_assign_scratch_bytes(int32_t n, int32_t g);
 int mux_assign(int32_t method, const double* weights, const int64_t* ids, int32_t n,
-               int32_t g, int32_t* out, void* scratch, void* stream);
+               int32_t g, int32_t* out, void* init_loads, void* stream);
 
-/* Segment copy: table = plan (dispatch: which=0, return: which=1).
+/* Segment copy: table = plan (dispatch: which=0, return: which=1,
+ * gradient return: which=2 with src_bases[group] = the dY buffer (LLM rows,
+ * row_bytes_ret wide) and dst_bases[rank * MUX_N_GROUPS + group]).
  * src_bases[group], dst_bases[rank * MUX_N_GROUPS + group] (dispatch) or
  * dst_bases[rank] (return) are device arrays of device pointers (local or
  * NVLink-peer).  Row bytes come from the plan cfg.  CTAs grab chunks from a

@@ -115,3 +115,26 @@ def dispatch_by_rank(plan: dict, lens, me: int):
             out.append((int(plan["arena_off"][i]), int(plan["enc_off"][i]), int(lens[i]),
                         int(plan["group"][i]), int(plan["enc"][i])))
     return np.array(out, np.int64).reshape(-1, 5)
+
+
+def grad_by_rank(plan: dict, me: int):
+    """Gradient-return segments of LLM rank `me` (the gradient path
+    of restore_order): (src LLM row on me, dst encoder row, rows, group, encoder
+    rank), in table order and, within a sample, in token order."""
+    out = []
+    for (i, src, dst_rank, dst_row, n) in plan["pieces"]:
+        if dst_rank == me and n > 0:
+            out.append((dst_row, src, n, int(plan["group"][i]), int(plan["enc"][i])))
+    return np.array(out, np.int64).reshape(-1, 5)
+
+
+def run_grad(plan: dict, world: int, dy, d_row):
+    """dY rows of every LLM rank [llm_rows[r], d_row] -> each encoder rank's
+    gradient buffer per group [recv_rows[e][g], d_row] in encoder order."""
+    G = plan["recv_rows"].shape[1]
+    grad = [[np.zeros((int(plan["recv_rows"][e, g]), d_row), dy[0].dtype) for g in range(G)]
+            for e in range(world)]
+    for (i, src, dst_rank, dst_row, n) in plan["pieces"]:
+        g, e = int(plan["group"][i]), int(plan["enc"][i])
+        grad[e][g][src:src + n] = dy[dst_rank][dst_row:dst_row + n]
+    return grad

@@ -284,3 +284,60 @@ def step_table(carry_seqs, drawn, chunk_sizes, modality_of):
     return dict(lens=np.array(lens, np.int64), mods=np.array(mods, np.int64),
                 ids=np.array(ids, np.int64), carry_seq=np.array(carry_seq, np.int64),
                 n_carry_seqs=len(carry_seqs), chunk_off=chunk_off)
+
+
+def plan_reshard(sequences, n_ranks, variant, cp_threshold=None, capacity=None):
+    """Encoder -> LLM shard map, one sequence at a time.
+
+    sequences: list of span lists [(sample id, tokens)].
+    UlyssesUniform: each sequence's fill F splits into n_ranks contiguous
+      shards, the first F mod n_ranks one token longer (pinned in
+      SURVEY.md §8.1-6); a sample maps to every shard its token range touches.
+    CpHybrid: samples longer than cp_threshold (default capacity / n_ranks,
+      SPEC.md:497) split into n_ranks near-equal pieces (same rule), one per
+      rank; shorter samples go whole to a rank by LPT whose initial loads are
+      the long-sample pieces already on each rank.
+    Returns {sample id: [(rank, start, end)]} (token ranges within the sample)
+    and per-rank token counts per sequence.
+    """
+    smap, loads = {}, []
+    for spans in sequences:
+        if variant == "ulysses":
+            F = sum(t for _, t in spans)
+            lens = ulysses_split(F, n_ranks)
+            starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+            pos = 0
+            for sid, t in spans:
+                pieces = []
+                for k in range(n_ranks):
+                    a, b = max(pos, int(starts[k])), min(pos + t, int(starts[k]) + lens[k])
+                    if a < b:
+                        pieces.append((k, a - pos, b - pos))
+                smap[sid] = pieces
+                pos += t
+            loads.append(list(lens))
+        elif variant == "cp_hybrid":
+            thr = cp_threshold if cp_threshold is not None else capacity // n_ranks
+            load = [0] * n_ranks
+            short = []
+            for idx, (sid, t) in enumerate(spans):
+                if t > thr:
+                    parts = ulysses_split(t, n_ranks)
+                    off = 0
+                    smap[sid] = []
+                    for k, n in enumerate(parts):
+                        smap[sid].append((k, off, off + n))
+                        load[k] += n
+                        off += n
+                else:
+                    short.append((idx, sid, t))
+            if short:
+                ranks = lpt_assign([float(t) for _, _, t in short], [sid for _, sid, _ in short],
+                                   n_ranks, init=[float(x) for x in load])
+                for (idx, sid, t), r in zip(short, ranks):
+                    smap[sid] = [(r, 0, t)]
+                    load[r] += t
+            loads.append(load)
+        else:
+            raise ValueError(f"unknown reshard variant {variant!r}")
+    return smap, loads

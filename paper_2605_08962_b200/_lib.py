@@ -21,6 +21,7 @@ H_STATUS, H_ERR_INDEX, H_N_SEQ, H_N_DISPATCH, H_N_RETURN = 0, 1, 2, 3, 4
 H_DISPATCH_CHUNKS, H_RETURN_CHUNKS, H_DISPATCH_BYTES, H_RETURN_BYTES = 5, 6, 7, 8
 H_N_BATCH, H_DISPATCH_REMOTE, H_RETURN_REMOTE, H_RECV_ROWS0, H_RECV_ROWS1 = 9, 10, 11, 12, 13
 H_STAGE_ROWS0, H_STAGE_ROWS1 = 14, 15
+H_N_GRAD, H_GRAD_CHUNKS, H_GRAD_BYTES, H_GRAD_REMOTE, H_STAMP0 = 16, 17, 18, 19, 20
 RET_FINAL, RET_STAGED = 0, 1
 H_SLOTS = 32
 
@@ -30,7 +31,8 @@ class PlanCfg(C.Structure):
         "S", "n_carry", "n_carry_seqs", "n_chunks", "capacity", "gbs", "dp", "sp", "world",
         "mbs", "method", "pooled", "me", "mode")] + [
         ("row_bytes_in", C.c_int32 * N_GROUPS), ("row_bytes_ret", C.c_int32 * N_GROUPS),
-        ("chunk_bytes", C.c_int32), ("ret_mode", C.c_int32)]
+        ("chunk_bytes", C.c_int32), ("ret_mode", C.c_int32),
+        ("row_bytes_grad", C.c_int32 * N_GROUPS)]
 
 
 LAYOUT_FIELDS = (
@@ -39,7 +41,8 @@ LAYOUT_FIELDS = (
     "chunk_err", "fills", "nspans", "cu", "shard_len", "shard_start", "row_base", "arena_rows",
     "recv_rows", "stage_rows", "llm_rows", "order", "scratch_a", "scratch_b", "dseg_src_row", "dseg_dst_row",
     "dseg_rows", "dseg_group", "dseg_dst_rank", "dseg_chunk0", "rseg_src_row", "rseg_dst_row",
-    "rseg_rows", "rseg_group", "rseg_dst_rank", "rseg_chunk0", "total")
+    "rseg_rows", "rseg_group", "rseg_dst_rank", "rseg_chunk0", "gseg_src_row", "gseg_dst_row",
+    "gseg_rows", "gseg_group", "gseg_dst_rank", "gseg_chunk0", "total")
 
 
 class PlanLayout(C.Structure):

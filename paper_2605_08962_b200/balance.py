@@ -27,7 +27,7 @@ from .planner import _stream_ptr
 from .workload import GlobalBatch, Sample
 
 
-def _assign(method: int, weights, g: int, ids=None) -> list[int]:
+def _assign(method: int, weights, g: int, ids=None, init=None) -> list[int]:
     if g < 1:
         raise ValueError("g must be >= 1")
     w = np.asarray(list(weights), dtype=np.float64)
@@ -40,8 +40,14 @@ def _assign(method: int, weights, g: int, ids=None) -> list[int]:
     idd = torch.from_numpy(np.asarray(ids if ids is not None else np.arange(w.size),
                                       dtype=np.int64)).to(dev)
     out = torch.empty(w.size, dtype=torch.int32, device=dev)
+    ini = None
+    if init is not None:
+        ini = torch.tensor([float(x) for x in init], dtype=torch.float64, device=dev)
+        if ini.numel() != g:
+            raise ValueError("init must hold one load per group")
     _lib.check(_lib.lib().mux_assign(method, wd.data_ptr(), idd.data_ptr(), int(w.size), int(g),
-                                     out.data_ptr(), None, _stream_ptr()), "mux_assign")
+                                     out.data_ptr(), None if ini is None else ini.data_ptr(),
+                                     _stream_ptr()), "mux_assign")
     return out.cpu().tolist()
 
 
@@ -54,9 +60,10 @@ def kk_partition(weights, g: int) -> list[int]:
     return _assign(_lib.KK, weights, g)
 
 
-def lpt_partition(weights, g: int, ids=None) -> list[int]:
-    """Greedy LPT: heaviest first (ties by id, then index) to the least-loaded rank."""
-    return _assign(_lib.LPT, weights, g, ids)
+def lpt_partition(weights, g: int, ids=None, init=None) -> list[int]:
+    """Greedy LPT: heaviest first (ties by id, then index) to the least-loaded rank;
+    `init`: loads the g ranks start with."""
+    return _assign(_lib.LPT, weights, g, ids, init)
 
 
 @dataclass

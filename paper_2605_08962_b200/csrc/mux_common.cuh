@@ -119,6 +119,8 @@ struct Plan {
   int32_t *dgroup, *drank;
   int64_t *rsrc, *rdst, *rrows, *rchunk0;
   int32_t *rgroup, *rrank;
+  int64_t *gsrc, *gdst, *grows, *gchunk0;
+  int32_t *ggroup, *grank;
 };
 
 Plan make_plan(void* base, const mux_plan_layout& L);

@@ -119,6 +119,12 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->rseg_group = take(4 * R);
   L->rseg_dst_rank = take(4 * R);
   L->rseg_chunk0 = take(8 * (R + 1));
+  L->gseg_src_row = take(8 * R);
+  L->gseg_dst_row = take(8 * R);
+  L->gseg_rows = take(8 * R);
+  L->gseg_group = take(4 * R);
+  L->gseg_dst_rank = take(4 * R);
+  L->gseg_chunk0 = take(8 * (R + 1));
   L->total = o;
   return MUX_OK;
 }
@@ -174,6 +180,12 @@ Plan make_plan(void* b, const mux_plan_layout& L) {
   p.rgroup = at<int32_t>(b, L.rseg_group);
   p.rrank = at<int32_t>(b, L.rseg_dst_rank);
   p.rchunk0 = at<int64_t>(b, L.rseg_chunk0);
+  p.gsrc = at<int64_t>(b, L.gseg_src_row);
+  p.gdst = at<int64_t>(b, L.gseg_dst_row);
+  p.grows = at<int64_t>(b, L.gseg_rows);
+  p.ggroup = at<int32_t>(b, L.gseg_group);
+  p.grank = at<int32_t>(b, L.gseg_dst_rank);
+  p.gchunk0 = at<int64_t>(b, L.gseg_chunk0);
   return p;
 }
 
@@ -186,7 +198,7 @@ __device__ __forceinline__ void stamp(Plan& p, int slot) {
   if (threadIdx.x == 0) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.hdr[slot] = (int64_t)t;
+    p.hdr[MUX_H_STAMP0 + slot - 16] = (int64_t)t;
   }
 }
 
@@ -224,9 +236,10 @@ struct PoolKey {  // (pool, -cost, id, table index) ascending; padding last
 };
 
 // Sequential LPT over sorted items by one warp; out[k] = rank of item k.
-__device__ void lpt_warp(const int* s_ord, const double* cost, int n, int g, int32_t* out_rank) {
+__device__ void lpt_warp(const int* s_ord, const double* cost, int n, int g, int32_t* out_rank,
+                         const double* init = nullptr) {
   const int lane = threadIdx.x & 31;
-  double load = 0.0;
+  double load = init != nullptr && lane < g ? init[lane] : 0.0;
   int nxt = n > 0 ? s_ord[0] : 0;
   double nc = n > 0 ? cost[nxt] : 0.0;
   for (int q = 0; q < n; ++q) {
@@ -994,6 +1007,10 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
   const int64_t CH = cfg.chunk_bytes > 0 ? cfg.chunk_bytes : kDefaultChunkBytes;
   int64_t dcarry = 0, rcarry = 0, dchunks = 0, rchunks = 0;
   int64_t dbytes = 0, rbytes = 0, dremote = 0, rremote = 0;
+  int64_t gcarry = 0, gchunks = 0, gbytes = 0, gremote = 0;
+  int grad_rb[MUX_N_GROUPS];
+  for (int q2 = 0; q2 < MUX_N_GROUPS; ++q2)
+    grad_rb[q2] = cfg.row_bytes_grad[q2] > 0 ? cfg.row_bytes_grad[q2] : cfg.row_bytes_ret[q2];
   for (int base = 0; base < S; base += nt) {
     const int i = base + tid;
     const bool e = i < S && enc_item(i);
@@ -1066,14 +1083,61 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
     }
     rcarry += tot;
     rchunks += tchk;
+    // gradient pieces: my LLM rows of this sample, back to its encoder rank
+    int gp = 0;
+    int64_t gchk = 0;
+    for (int t = 0; e && L > 0 && t < L;) {
+      const int pos = off + t, kk = owner_k(q, pos);
+      const int end = s_sstart[q * sp + kk] + s_slen[q * sp + kk];
+      const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
+      if ((q / P) * sp + kk == me) {
+        ++gp;
+        gchk += ((int64_t)n * grad_rb[g] + CH - 1) / CH;
+      }
+      t += n;
+    }
+    const int64_t gslot = block_excl_scan(gp, &tot, s_warp);
+    const int64_t gchk_pre = block_excl_scan(gchk, &tchk, s_warp);
+    if (gp) {
+      int slot2 = (int)(gcarry + gslot);
+      int64_t c1 = gchunks + gchk_pre;
+      for (int t = 0; t < L;) {
+        const int pos = off + t, kk = owner_k(q, pos);
+        const int end = s_sstart[q * sp + kk] + s_slen[q * sp + kk];
+        const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
+        if ((q / P) * sp + kk == me) {
+          const int64_t nb = (int64_t)n * grad_rb[g];
+          p.gsrc[slot2] = p.row_base[q * sp + kk] + pos - s_sstart[q * sp + kk];
+          p.gdst[slot2] = w.eoff[i] + t;
+          p.grows[slot2] = n;
+          p.ggroup[slot2] = g;
+          p.grank[slot2] = w.enc[i];
+          p.gchunk0[slot2] = c1;
+          c1 += (nb + CH - 1) / CH;
+          gbytes += nb;
+          if (w.enc[i] != me) gremote += nb;
+          ++slot2;
+        }
+        t += n;
+      }
+    }
+    gcarry += tot;
+    gchunks += tchk;
   }
   {
-    int64_t t0, t1, t2, t3;
+    int64_t t0, t1, t2, t3, t4, t5;
     block_excl_scan(dbytes, &t0, s_warp);
     block_excl_scan(rbytes, &t1, s_warp);
     block_excl_scan(dremote, &t2, s_warp);
     block_excl_scan(rremote, &t3, s_warp);
+    block_excl_scan(gbytes, &t4, s_warp);
+    block_excl_scan(gremote, &t5, s_warp);
     if (tid == 0) {
+      p.gchunk0[gcarry] = gchunks;
+      p.hdr[MUX_H_N_GRAD] = gcarry;
+      p.hdr[MUX_H_GRAD_CHUNKS] = gchunks;
+      p.hdr[MUX_H_GRAD_BYTES] = t4;
+      p.hdr[MUX_H_GRAD_REMOTE] = t5;
       p.dchunk0[dcarry] = dchunks;
       p.rchunk0[rcarry] = rchunks;
       p.hdr[MUX_H_DISPATCH_CHUNKS] = dchunks;
@@ -1122,7 +1186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Stand-alone partition (kk_partition / LPT) of one pool.
 __global__ void __launch_bounds__(kThreads, 1) assign_kernel(int method, const double* w,
                                                              const int64_t* ids, int n, int g,
-                                                             int32_t* out) {
+                                                             int32_t* out, const double* init) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int npad = next_pow2(n > 0 ? n : 1);
   double* cost = reinterpret_cast<double*>(smem);
@@ -1145,7 +1209,7 @@ __global__ void __launch_bounds__(kThreads, 1) assign_kernel(int method, const d
     for (int k = threadIdx.x; k < n; k += blockDim.x) rank[k] = 0;
   } else if (method == MUX_LPT) {
     bitonic_sort(ord, npad, PoolKey{pool, cost, id, tidx, n});
-    if (threadIdx.x < 32) lpt_warp(ord, cost, n, g, rank);
+    if (threadIdx.x < 32) lpt_warp(ord, cost, n, g, rank, init);
   } else {
     KkSmem& K = *reinterpret_cast<KkSmem*>(smem + align_up(32 * npad, 16));
     if (threadIdx.x < 32) kk_warp(K, cost, n, g, rank);
@@ -1254,7 +1318,11 @@ extern "C" int mux_plan_check(const mux_plan_cfg* cfg, const int64_t* h, const i
 extern "C" size_t mux_assign_scratch_bytes(int32_t, int32_t) { return 0; }
 
 extern "C" int mux_assign(int32_t method, const double* w, const int64_t* ids, int32_t n,
-                          int32_t g, int32_t* out, void*, void* stream) {
+                          int32_t g, int32_t* out, void* init_loads, void* stream) {
+  if (init_loads != nullptr && method != MUX_LPT) {
+    set_error("initial loads are only defined for LPT");
+    return MUX_ERR_VALUE;
+  }
   if (g < 1 || g > 8) {
     set_error("group count %d outside 1..8", g);
     return MUX_ERR_VALUE;
@@ -1269,8 +1337,8 @@ extern "C" int mux_assign(int32_t method, const double* w, const int64_t* ids, i
   const int smem = (int)align_up(32 * npad, 16) + (method == MUX_KK ? (int)sizeof(KkSmem) : 0);
   MUX_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemLimit));
-  assign_kernel<<<1, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(method, w, ids, n, g,
-                                                                          out);
+  assign_kernel<<<1, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      method, w, ids, n, g, out, static_cast<const double*>(init_loads));
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

@@ -352,19 +352,27 @@ extern "C" int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t
   if (st) return st;
   Plan p = make_plan_const(plan, L);
   SegArgs a;
+  if (which < 0 || which > 2) {
+    set_error("segment table %d: 0 dispatch, 1 return, 2 gradient return", which);
+    return MUX_ERR_VALUE;
+  }
   const bool ret = which != 0;
-  a.hdr_chunks = p.hdr + (ret ? MUX_H_RETURN_CHUNKS : MUX_H_DISPATCH_CHUNKS);
-  a.hdr_segs = p.hdr + (ret ? MUX_H_N_RETURN : MUX_H_N_DISPATCH);
-  a.chunk0 = ret ? p.rchunk0 : p.dchunk0;
-  a.src_row = ret ? p.rsrc : p.dsrc;
-  a.dst_row = ret ? p.rdst : p.ddst;
-  a.rows = ret ? p.rrows : p.drows;
-  a.group = ret ? p.rgroup : p.dgroup;
-  a.rank = ret ? p.rrank : p.drank;
+  const bool grad = which == 2;
+  a.hdr_chunks = p.hdr + (grad ? MUX_H_GRAD_CHUNKS : ret ? MUX_H_RETURN_CHUNKS
+                                                         : MUX_H_DISPATCH_CHUNKS);
+  a.hdr_segs = p.hdr + (grad ? MUX_H_N_GRAD : ret ? MUX_H_N_RETURN : MUX_H_N_DISPATCH);
+  a.chunk0 = grad ? p.gchunk0 : ret ? p.rchunk0 : p.dchunk0;
+  a.src_row = grad ? p.gsrc : ret ? p.rsrc : p.dsrc;
+  a.dst_row = grad ? p.gdst : ret ? p.rdst : p.ddst;
+  a.rows = grad ? p.grows : ret ? p.rrows : p.drows;
+  a.group = grad ? p.ggroup : ret ? p.rgroup : p.dgroup;
+  a.rank = grad ? p.grank : ret ? p.rrank : p.drank;
   a.chunk_bytes = cfg->chunk_bytes > 0 ? cfg->chunk_bytes : kDefaultChunkBytes;
   for (int g = 0; g < MUX_N_GROUPS; ++g)
-    a.row_bytes[g] = ret ? cfg->row_bytes_ret[g] : cfg->row_bytes_in[g];
-  a.per_group_dst = (!ret || cfg->ret_mode == MUX_RET_STAGED) ? 1 : 0;
+    a.row_bytes[g] = grad ? (cfg->row_bytes_grad[g] > 0 ? cfg->row_bytes_grad[g]
+                                                        : cfg->row_bytes_ret[g])
+                          : ret ? cfg->row_bytes_ret[g] : cfg->row_bytes_in[g];
+  a.per_group_dst = (!ret || grad || cfg->ret_mode == MUX_RET_STAGED) ? 1 : 0;
   a.src_bases = src_bases;
   a.dst_bases = dst_bases;
   a.flags_peers = flags_peers;

@@ -114,7 +114,7 @@ class MuxPath:
         self.flags.tensor.zero_()
         self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
                         for g in range(N_GROUPS)]
-        self.sync = torch.zeros(4, dtype=torch.int32, device=dev)  # copy counters x2
+        self.sync = torch.zeros(6, dtype=torch.int32, device=dev)  # copy counters x3 tables
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
@@ -156,7 +156,8 @@ class MuxPath:
         return make_cfg(table, self.capacity, self.gbs, self.dp, self.sp, self.world, 1,
                         self.method, self.pooled, self.rank,
                         row_bytes_in=tuple(2 * d for d in self.d_in),
-                        row_bytes_ret=tuple(2 * d for d in self.d_ret), ret_mode=self.ret_mode)
+                        row_bytes_ret=tuple(2 * d for d in self.d_ret), ret_mode=self.ret_mode,
+                        row_bytes_grad=(2 * self.d_llm,) * N_GROUPS)
 
     @property
     def llm(self) -> _Window:
@@ -340,6 +341,55 @@ class MuxPath:
         self._ev_p[b] = ev_p
         self.last_llm = b
         return ev_p
+
+    # --------------------------------------------------------- gradient return
+    def _ensure_grad(self):
+        if getattr(self, "grad", None) is None:
+            dev, w = self.device, self.world
+            width = self.d_llm  # dL/d(projector output or returned rows): d_llm wide
+            self.grad = [_Window(self.max_rows * width * 2, dev, self.group, w)
+                         for _ in range(N_GROUPS)]
+            self.grad_dst = _ptr_table([self.grad[g].ptrs[r] for r in range(w)
+                                        for g in range(N_GROUPS)], dev)
+            self._dy_tables: dict = {}
+            if w > 1:
+                torch.cuda.synchronize()
+                self.flags.handle.barrier()
+
+    def grad_return(self, plan: Plan, dy: torch.Tensor, stream=None):
+        """Backward of return + scatter (restore_order on the
+        gradient path): this rank's dY rows at the placeholder positions of its
+        packed LLM input go back to the encoder ranks, in encoder order, into
+        `grad_view(g, rows)`.  dy: [>= llm rows, d_llm] bf16 on this GPU.
+        With the projector, dX = dY W and dW = dY^T X then run on the encoder
+        rank (`projector_backward`)."""
+        if self.ret_mode != _lib.RET_FINAL:
+            raise ValueError("gradient return is defined for the final-row layouts")
+        assert dy.dtype == torch.bfloat16 and dy.shape[-1] == self.d_llm and dy.is_contiguous()
+        self._ensure_grad()
+        key = dy.data_ptr()
+        t = self._dy_tables.get(key)
+        if t is None:
+            t = _ptr_table([key] * N_GROUPS, self.device)
+            self._dy_tables[key] = t
+        self._exchange(plan, 2, t, self.grad_dst, stream)
+
+    def projector_backward(self, group: int, rows: int, x: torch.Tensor | None = None):
+        """dX = dY W and dW = dY^T X for encoder group `group` on this encoder rank,
+        from the returned gradient rows (plain GEMMs: cuBLAS through torch).
+        x: the projector inputs [rows, d_enc] (default: this rank's encoder output)."""
+        assert self.projector and self.weight[group] is not None
+        dy = self.grad_view(group, rows)
+        x = self.enc_view(group, rows) if x is None else x
+        dx = dy @ self.weight[group]
+        dw = dy.t() @ x
+        db = dy.float().sum(0).to(torch.bfloat16)
+        return dx, dw, db
+
+    def grad_view(self, group: int, rows: int) -> torch.Tensor:
+        self._ensure_grad()
+        return self.grad[group].tensor[: rows * self.d_llm * 2].view(torch.bfloat16).view(
+            rows, self.d_llm)
 
     def finish(self, stream=None):
         """Make `stream` wait for every outstanding overlapped projector."""

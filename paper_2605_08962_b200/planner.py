@@ -117,7 +117,7 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
              world: int = 1, mbs: int = 1, method: str = "lpt", pooled: bool = False,
              me: int = 0, mode: int = _lib.MODE_STEP, row_bytes_in=(1176, 1024),
              row_bytes_ret=(8192, 8192), chunk_bytes: int = DEFAULT_CHUNK_BYTES,
-             ret_mode: int = _lib.RET_FINAL) -> PlanCfg:
+             ret_mode: int = _lib.RET_FINAL, row_bytes_grad=None) -> PlanCfg:
     if method not in METHODS:
         raise ValueError(f"unknown balance method {method!r}")
     c = PlanCfg()
@@ -130,6 +130,8 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
         c.row_bytes_ret[g] = row_bytes_ret[g]
     c.chunk_bytes = chunk_bytes
     c.ret_mode = ret_mode
+    for g in range(_lib.N_GROUPS):
+        c.row_bytes_grad[g] = 0 if row_bytes_grad is None else row_bytes_grad[g]
     return c
 
 
@@ -144,10 +146,12 @@ class Plan:
 
     I32 = ("seq", "off", "span", "origin", "origin_pos", "group", "enc", "llm_rank",
            "bin_of", "fills", "nspans", "cu", "shard_len", "shard_start", "dseg_group",
-           "dseg_dst_rank", "rseg_group", "rseg_dst_rank", "chunk_nbins")
+           "dseg_dst_rank", "rseg_group", "rseg_dst_rank", "chunk_nbins", "gseg_group",
+           "gseg_dst_rank")
     I64 = ("arena_off", "enc_off", "llm_row", "row_base", "arena_rows", "recv_rows", "llm_rows",
            "dseg_src_row", "dseg_dst_row", "dseg_rows", "rseg_src_row", "rseg_dst_row",
-           "rseg_rows", "dseg_chunk0", "rseg_chunk0")
+           "rseg_rows", "dseg_chunk0", "rseg_chunk0", "gseg_src_row", "gseg_dst_row",
+           "gseg_rows", "gseg_chunk0")
 
     def __init__(self, cfg: PlanCfg, device, blob: torch.Tensor | None = None):
         self.cfg = cfg
@@ -200,6 +204,10 @@ class Plan:
             out["recv_rows"] = self.view("recv_rows", W * G).cpu().numpy().reshape(W, G)
             out["llm_rows"] = self.view("llm_rows", W).cpu().numpy()
             nd, nr = int(h[_lib.H_N_DISPATCH]), int(h[_lib.H_N_RETURN])
+            ng = int(h[_lib.H_N_GRAD])
+            out["gseg"] = np.stack([self.view(k, ng).cpu().numpy().astype(np.int64) for k in (
+                "gseg_src_row", "gseg_dst_row", "gseg_rows", "gseg_group", "gseg_dst_rank")],
+                axis=1) if ng else np.zeros((0, 5), np.int64)
             out["dseg"] = np.stack([self.view("dseg_src_row", nd).cpu().numpy(),
                                     self.view("dseg_dst_row", nd).cpu().numpy(),
                                     self.view("dseg_rows", nd).cpu().numpy(),

@@ -17,8 +17,7 @@ cfg, dp, sp, gbs = bench.workload(name, world)
 tables = bench.generate_steps(name, world, 4)
 path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=0,
                d_in=configs.D_IN, d_llm=configs.D_LLM, max_rows=gbs * configs.CAPACITY)
-names = ["ffd(start->fin start)", "A-B", "C", "D", "E", "F", "G (assign)", "H", "I (pieces/segs)",
-         "chunk maps"]
+names = ["ffd(start->fin start)", "A-B", "C", "D", "E", "F", "G (assign)", "H", "H2+I (segments)"]
 acc = []
 for rep in range(20):
     for t in tables:
@@ -26,7 +25,7 @@ for rep in range(20):
         p = path.plan(dt)
         torch.cuda.synchronize()
         h = p.header()
-        ts = [h[16], h[17], h[18], h[19], h[20], h[21], h[22], h[23], h[24], h[26], h[25]]
+        ts = [h[20 + x - 16] for x in (16, 17, 18, 19, 20, 21, 22, 23, 24, 25)]
         acc.append(np.diff(np.array(ts, dtype=np.float64)) / 1e3)
 a = np.array(acc[8:])
 print(f"{name} world={world}: S={[t.S for t in tables]}")

@@ -128,6 +128,22 @@ def main():
             if not np.array_equal(got, llm[rank]):
                 print(f"rank {rank} step {step} {method}: llm buffer differs", flush=True)
                 fails += 1
+            # gradient return: every rank's dY rows back to the encoder ranks
+            dys = [payload(max(int(o["llm_rows"][r]), 1), d_llm, 5000 + 10 * step + r)
+                   for r in range(world)]
+            dist.barrier()
+            path.grad_return(plan, dys[rank].to(dev))
+            torch.cuda.synchronize()
+            path.check_wait()
+            want = odp.run_grad(o, world, [d.view(torch.int16).numpy().view(np.uint16)
+                                           for d in dys], d_llm)
+            for g in range(2):
+                r_ = int(o["recv_rows"][rank, g])
+                got = path.grad_view(g, r_).cpu().view(torch.int16).numpy().view(np.uint16)
+                if not np.array_equal(got, want[rank][g]):
+                    print(f"rank {rank} step {step} {method}: gradient group {g} differs",
+                          flush=True)
+                    fails += 1
             moved = int(o["recv_rows"].sum())
             if rank == 0:
                 print(f"step {step} {method}: {moved} modality tokens over {world} ranks ok="

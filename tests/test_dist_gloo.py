@@ -1,0 +1,95 @@
+"""The multi-rank protocol on CPU (gloo, world size 2): every rank plans the
+whole step on its own, derives its own segment tables, pushes its rows, and the
+ranks end up with exactly the oracle's per-rank buffers — with no counts
+exchanged.  This is the host-side logic of the NVLink push exchange; the GPU
+tests run the same protocol with the CUDA kernels (tests/mgpu_worker.py)."""
+
+import hashlib
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import dataplane as odp
+from oracle import planner as oplan
+from tests.helpers import golden_steps
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _digest(plan):
+    h = hashlib.sha256()
+    for k in ("seq", "off", "origin", "enc", "arena_off", "enc_off", "recv_rows", "llm_rows"):
+        h.update(np.ascontiguousarray(plan[k]).tobytes())
+    h.update(repr(plan["pieces"]).encode())
+    return h.hexdigest()
+
+
+def _worker(rank, world, port, cases, result_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok = True
+    for t, st, d_in, d_llm in cases:
+        plan = oplan.plan_step(t, 16384, st["gbs"], st["dp"], world // st["dp"], world)
+        digests = [None] * world
+        dist.all_gather_object(digests, _digest(plan))
+        ok &= len(set(digests)) == 1  # every rank computed the identical plan
+        # every rank's loader arena is seeded, so the oracle can rebuild all ranks
+        g = np.random.default_rng(7)
+        arenas = [[g.integers(0, 2 ** 16, size=(int(plan["arena_rows"][r, q]), d_in[q]),
+                              dtype=np.uint16) for q in range(2)] for r in range(world)]
+        # dispatch: my segments, pushed as (dst rank, group, dst row, rows payload)
+        sends = [[] for _ in range(world)]
+        for src, dst, n, q, to in odp.dispatch_by_rank(plan, t["lens"], rank).tolist():
+            sends[to].append((q, dst, arenas[rank][q][src:src + n]))
+        got = [None] * world
+        dist.all_gather_object(got, sends)
+        recv = [np.zeros((int(plan["recv_rows"][rank, q]), d_in[q]), np.uint16) for q in range(2)]
+        for r in range(world):
+            for q, dst, rows in got[r][rank]:
+                recv[q][dst:dst + len(rows)] = rows
+        ref_recv, enc_out, ref_llm = odp.run_world(plan, t, world, arenas, d_in, (d_llm,) * 2,
+                                                   d_llm)
+        ok &= all(np.array_equal(recv[q], ref_recv[rank][q]) for q in range(2))
+        # return: my encoder rows to their LLM ranks
+        sends = [[] for _ in range(world)]
+        for src, dst, n, q, to in odp.pieces_by_rank(plan, rank).tolist():
+            sends[to].append((dst, enc_out[rank][q][src:src + n]))
+        got = [None] * world
+        dist.all_gather_object(got, sends)
+        llm = np.zeros((int(plan["llm_rows"][rank]), d_llm), np.uint16)
+        for r in range(world):
+            for dst, rows in got[r][rank]:
+                llm[dst:dst + len(rows)] = rows
+        ok &= np.array_equal(llm, ref_llm[rank])
+    result_q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_push_protocol_gloo(world):
+    cases = []
+    for name, st, t, _ in golden_steps():
+        if st["world"] == world and name in ("cfg5", "cfg3") and st["step"] < 2:
+            cases.append((t, st, (12, 4), 16))
+    assert cases
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}

@@ -47,6 +47,15 @@ def run_step(t, cap, gbs, d_in, d_llm, method="lpt", check_enc=True):
     n = int(o["llm_rows"][0])
     got = path.llm_view(n).cpu().view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(got, llm[0]), "packed LLM input"
+    # gradient path: dY at the placeholder rows back to encoder order
+    dy = payload(max(n, 1), d_llm, 7).cuda()
+    path.grad_return(plan, dy)
+    torch.cuda.synchronize()
+    want = odp.run_grad(o, 1, [dy.cpu().view(torch.int16).numpy().view(np.uint16)], d_llm)
+    for g in range(2):
+        r = int(o["recv_rows"][0, g])
+        got = path.grad_view(g, r).cpu().view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got, want[0][g]), f"gradient return group {g}"
     return o
 
 

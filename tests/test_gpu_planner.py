@@ -45,6 +45,7 @@ def assert_plan_equal(d, o, t, me):
     assert np.array_equal(d["row_base"].reshape(o["row_base"].shape), o["row_base"])
     assert np.array_equal(d["dseg"], odp.dispatch_by_rank(o, t["lens"], me))
     assert np.array_equal(d["rseg"], odp.pieces_by_rank(o, me))
+    assert np.array_equal(d["gseg"], odp.grad_by_rank(o, me))
 
 
 @pytest.mark.parametrize("method", ["lpt", "kk"])
@@ -148,3 +149,52 @@ def test_partition_matches_oracle(cuda_device, method):
             got = balance.lpt_partition(w, g, ids=ids)
         assert list(got) == list(want)
     assert list(balance.kk_partition([8, 7, 6, 5, 4], 2)) == [1, 0, 1, 0, 0]
+
+
+def test_plan_reshard_matches_oracle(cuda_device):
+    from paper_2605_08962_b200 import reshard
+    from paper_2605_08962_b200 import costs
+    for name, st, t, _ in golden_steps():
+        if st["world"] != 1:
+            continue
+        seqs = [W.PackedSequence(configs.CAPACITY, [tuple(x) for x in q]) for q in st["batch"]]
+        raw = [[tuple(x) for x in q] for q in st["batch"]]
+        for sp in (2, 4, 8):
+            got = reshard.plan_reshard(seqs, sp, "ulysses")
+            want, loads = oplan.plan_reshard(raw, sp, "ulysses")
+            assert got.shard_map == want and got.tokens_per_rank == loads
+        for cp, thr in ((2, None), (4, 4096), (4, 1024)):
+            got = reshard.plan_reshard(seqs, cp, "cp_hybrid", cp_threshold=thr)
+            want, loads = oplan.plan_reshard(raw, cp, "cp_hybrid", cp_threshold=thr,
+                                             capacity=configs.CAPACITY)
+            assert got.shard_map == want and got.tokens_per_rank == loads
+            ev, sec = reshard.dispatch_cost(got, costs.CommModel())
+            assert sec > 0 and len(ev) == len(seqs)
+    assert reshard.dispatch_cost(reshard.ReshardPlan("ulysses"), costs.CommModel()) == ([], 0.0)
+
+
+def test_grouped_reorder_and_restore(cuda_device):
+    # [10,1,1,1] over 4 ranks -> max stays 10, imbalance 10/3.25;
+    # reorder then restore == original order, for KK and LPT
+    for method in ("kk", "lpt"):
+        g = balance.ReorderGroup([0, 1, 2, 3], [[W.Sample(i, W.Modality.IMAGE, "x", L)]
+                                                for i, L in enumerate([10, 1, 1, 1])])
+        out, rec = balance.grouped_reorder(g, 1, method)
+        loads = [sum(s.length for s in lst) for lst in out]
+        assert max(loads) == 10 and balance.imbalance(loads) == 10 / 3.25
+        back = balance.restore_order(rec, out)
+        assert [[s.id for s in lst] for lst in back] == [[0], [1], [2], [3]]
+    rs = np.random.RandomState(4)
+    lists = [[W.Sample(100 * r + j, W.Modality.AUDIO, "x", int(rs.randint(1, 5000)))
+              for j in range(int(rs.randint(0, 9)))] for r in range(4)]
+    lists[0] += [W.Sample(999 + j, W.Modality.VIDEO, "x", 16000) for j in range(4)]  # skewed rank
+    pre = [sum(s.length for s in lst) for lst in lists]
+    out, rec = balance.grouped_reorder(balance.ReorderGroup([0, 1, 2, 3], lists), 2, "kk")
+    post = [sum(s.length for s in lst) for lst in out]
+    assert balance.imbalance(post) < balance.imbalance(pre)
+    back = balance.restore_order(rec, out)
+    assert [[s.id for s in lst] for lst in back] == [[s.id for s in lst] for lst in lists]
+    with pytest.raises(ValueError):
+        bad = balance.ReorderRecord(forward={(0, 0): (0, 0), (0, 1): (0, 0)}, shape=[2])
+        balance.restore_order(bad, [[1, 2]])
+    assert balance.zero_redundancy_filter(None, 1, 4, 16) == [1, 5, 9, 13]

@@ -159,3 +159,39 @@ def test_random_tables_plan_runs():
             except ValueError:
                 continue
             assert (p["origin"][p["in_batch"]] >= 0).all()
+
+
+def test_reshard_spec_kats():
+    # one 16K sequence, Ulysses sp=4 -> 4 shards of 4K
+    smap, loads = oplan.plan_reshard([[(7, 16384)]], 4, "ulysses")
+    assert loads == [[4096] * 4]
+    assert smap[7] == [(0, 0, 4096), (1, 4096, 8192), (2, 8192, 12288), (3, 12288, 16384)]
+    # CpHybrid [9000, 1024, 512], cp=4, threshold 4096 -> 9000 in 4 x 2250
+    smap, loads = oplan.plan_reshard([[(1, 9000), (2, 1024), (3, 512)]], 4, "cp_hybrid",
+                                     cp_threshold=4096)
+    assert [e - s for _, s, e in smap[1]] == [2250] * 4
+    assert len(smap[2]) == 1 and len(smap[3]) == 1 and sum(loads[0]) == 10536
+    # all below threshold -> nothing sharded
+    smap, _ = oplan.plan_reshard([[(1, 900), (2, 100)]], 4, "cp_hybrid", cp_threshold=4096)
+    assert all(len(v) == 1 for v in smap.values())
+
+
+def test_reshard_invariants_on_golden_batches():
+    # token conservation, contiguous/disjoint cover, Ulysses
+    # symmetry +-1, threshold monotonicity
+    for name, st, t, _ in golden_steps():
+        seqs = [[tuple(x) for x in q] for q in st["batch"]]
+        for sp in (2, 4, 8):
+            smap, loads = oplan.plan_reshard(seqs, sp, "ulysses")
+            for q, l in zip(seqs, loads):
+                assert sum(l) == sum(x for _, x in q) and max(l) - min(l) <= 1
+            for sid, tok in (x for q in seqs for x in q):
+                cover = sorted((s, e) for _, s, e in smap[sid])
+                assert cover[0][0] == 0 and cover[-1][1] == tok
+                assert all(a[1] == b[0] for a, b in zip(cover, cover[1:]))
+        prev = None
+        for thr in (256, 1024, 4096, 16384):
+            smap, loads = oplan.plan_reshard(seqs, 4, "cp_hybrid", cp_threshold=thr)
+            n_sharded = sum(len(v) > 1 for v in smap.values())
+            assert prev is None or n_sharded <= prev
+            prev = n_sharded
