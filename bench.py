@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--stages", action="store_true", help="per-stage timing breakdown")
     ap.add_argument("--pipeline", type=int, default=1,
                     help="1: plan step k+1 on a side stream during step k (default)")
+    ap.add_argument("--method", default="lpt_local", choices=["lpt", "kk", "lpt_local"],
+                    help="encoder balancing: locality-first LPT (default), LPT or KK")
     ap.add_argument("--hang-dump", type=float, default=0.0,
                     help="dump Python stacks after this many seconds (debug)")
     ap.add_argument("--graphs", type=int, default=0,
@@ -219,7 +221,7 @@ def run_ours(args):
 
     path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
                    d_in=d_in, d_enc=d_enc, d_llm=d_llm, projector=projector, device=dev,
-                   group=group)
+                   group=group, method=args.method)
     if projector:
         gen = torch.Generator(device=dev).manual_seed(77)
         for g in range(2):
@@ -404,6 +406,7 @@ def run_ours(args):
                    "d_llm": d_llm, "distinct_steps": n_distinct,
                    "modality_tokens_per_step": M_total / args.steps,
                    "planner": "pipelined on a side stream" if args.pipeline else "in-line",
+                   "balance": args.method,
                    "launch": "one CUDA graph per step" if graphs is not None else "eager",
                    "llm_tokens_per_step": T_total / args.steps,
                    "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"},
@@ -415,7 +418,7 @@ def run_ours(args):
     if rank == 0:
         line["clocks"] = clk.summary()
         if world == 1:
-            line["cpu_baseline"] = cpu_baseline(name, tables[0], projector, world)
+            line["cpu_baseline"] = cpu_baseline(name, tables[0], projector, world, args.method)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -528,7 +531,7 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
 # CPU reference arm (oracle port; the reference itself never moves token data)
 # ----------------------------------------------------------------------------
 
-def cpu_baseline(name, table, projector, world=1):
+def cpu_baseline(name, table, projector, world=1, method="lpt_local"):
     """Time the CPU port on one step of the workload at `world` GPUs' scale.
 
     Code timed: the oracle planner (FFD + batch + LPT + reshard; restates the
@@ -551,7 +554,7 @@ def cpu_baseline(name, table, projector, world=1):
              chunk_off=table.chunk_off.tolist())
     d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, configs.D_LLM
     t0 = time.perf_counter()
-    o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world)
+    o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
     t_plan = time.perf_counter() - t0
     lens = t["lens"]
     items = np.flatnonzero(o["enc"] >= 0)
@@ -629,7 +632,8 @@ def run_reference(args):
     tables = generate_steps_host(name, world, max(1, min(args.steps + args.warmup, 4)))
     vals = []
     for k in range(args.warmup + args.steps):
-        r = cpu_baseline(name, tables[k % len(tables)], bool(cfg["projector"]), world)
+        r = cpu_baseline(name, tables[k % len(tables)], bool(cfg["projector"]), world,
+                         args.method)
         if k >= args.warmup:
             vals.append(r)
     v = float(np.mean([r["value"] for r in vals]))

@@ -50,6 +50,8 @@ extern "C" {
 
 #define MUX_LPT 0
 #define MUX_KK 1
+#define MUX_LPT_LOCAL 2 /* locality-first LPT: keep samples on their origin rank up to
+                           the balanced load, LPT the rest on top */
 
 #define MUX_N_GROUPS 2 /* encoder groups: 0 = vision (image/video), 1 = audio */
 
@@ -88,7 +90,7 @@ typedef struct {
   int32_t n_chunks;     /* drawn chunks after the carry samples             */
   int32_t capacity;
   int32_t gbs, dp, sp, world, mbs;
-  int32_t method;       /* MUX_LPT | MUX_KK                                 */
+  int32_t method;       /* MUX_LPT | MUX_KK | MUX_LPT_LOCAL                 */
   int32_t pooled;       /* 1: balance all modalities together */
   int32_t me;           /* rank whose segment tables are emitted            */
   int32_t mode;         /* MUX_MODE_PACK | MUX_MODE_STEP                    */

@@ -49,6 +49,35 @@ def lpt_assign(costs, ids, g, init=None):
     return out
 
 
+def lpt_local_assign(costs, ids, origins, g):
+    """Locality-first LPT (builder's variant of the north_star's greedy/LPT; the
+    reference balances with KK over the whole group, moving
+    almost every sample).  In LPT order (-cost, id, index): pass 1 keeps an item
+    on its origin rank while that rank's kept load plus the item stays within
+    T = sum(costs) / g; pass 2 places the remaining items by LPT (least load,
+    lowest rank) on top of the kept loads.  Costs are integer token counts, so
+    every sum is exact."""
+    n = len(costs)
+    order = sorted(range(n), key=lambda i: (-costs[i], ids[i], i))
+    T = float(sum(costs)) / g
+    kept = [0.0] * g
+    out = [0] * n
+    pool = []
+    for i in order:
+        o = origins[i]
+        if kept[o] + costs[i] <= T:
+            kept[o] = kept[o] + costs[i]
+            out[i] = o
+        else:
+            pool.append(i)
+    load = list(kept)
+    for i in pool:
+        r = min(range(g), key=lambda k: (load[k], k))
+        out[i] = r
+        load[r] = load[r] + costs[i]
+    return out
+
+
 def kk_assign(weights, g):
     """g-way Karmarkar-Karp largest differencing.
 
@@ -220,6 +249,9 @@ def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=F
             ranks = lpt_assign(costs, [int(ids[i]) for i in items], world)
         elif method == "kk":
             ranks = kk_assign(costs, world)
+        elif method == "lpt_local":
+            ranks = lpt_local_assign(costs, [int(ids[i]) for i in items],
+                                     [int(origin[i]) for i in items], world)
         else:
             raise ValueError(f"unknown method {method!r}")
         for i, r in zip(items, ranks):

@@ -266,6 +266,56 @@ __device__ void lpt_warp(const int* s_ord, const double* cost, int n, int g, int
   }
 }
 
+// Locality-first LPT over sorted items by one warp: pass 1 keeps each item on
+// its origin rank while that rank's kept load stays within the balanced load
+// T = sum / g; pass 2 places the rest by LPT on top of the kept loads.  With
+// integer-valued costs every sum is exact, so it matches the CPU oracle bit
+// for bit (oracle/planner.py:lpt_local_assign).
+__device__ void lpt_local_warp(const int* s_ord, const double* cost, const int32_t* origin, int n,
+                               int g, int32_t* out_rank, int32_t* s_kept_flag) {
+  const int lane = threadIdx.x & 31;
+  double part = 0.0;
+  for (int q = lane; q < n; q += 32) part += cost[s_ord[q]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(MUX_FULL, part, o);
+  const double T = __ddiv_rn(part, (double)g);
+  double kept = 0.0;  // lane k < g: kept load of rank k
+  for (int q = 0; q < n; ++q) {
+    const int k = s_ord[q];
+    const double c = cost[k];
+    const int o = origin[k];
+    const double ko = __shfl_sync(MUX_FULL, kept, o);
+    const bool keep = __dadd_rn(ko, c) <= T;
+    if (keep && lane == o) kept = __dadd_rn(kept, c);
+    if (lane == 0) {
+      s_kept_flag[q] = keep;
+      if (keep) out_rank[k] = o;
+    }
+  }
+  __syncwarp();
+  double load = kept;
+  for (int q = 0; q < n; ++q) {
+    if (s_kept_flag[q]) continue;
+    const int k = s_ord[q];
+    const double c = cost[k];
+    double l = lane < g ? load : __longlong_as_double(0x7ff0000000000000LL);
+    int r = lane;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const double l2 = __shfl_xor_sync(MUX_FULL, l, o, 8);
+      const int r2 = __shfl_xor_sync(MUX_FULL, r, o, 8);
+      if (l2 < l || (l2 == l && r2 < r)) {
+        l = l2;
+        r = r2;
+      }
+    }
+    r = __shfl_sync(MUX_FULL, r, 0);
+    if (lane == r) load = __dadd_rn(load, c);
+    if (lane == 0) out_rank[k] = r;
+  }
+  __syncwarp();
+}
+
 struct KkSmem {
   double sum[kKkMax * 8];
   int32_t mn[kKkMax * 8];
@@ -588,7 +638,7 @@ __host__ __device__ inline SmemPlan smem_plan(int S, int n_seq_max, int gb, int 
   L.lpt = o;  // phase E counters, then the pool sort (phase G)
   int spad = 1;
   while (spad < S) spad <<= 1;
-  o += 32 * spad > 8 * gb ? 32 * spad : 8 * gb;  // cost f64, id i64, tidx, pool, ord, rank
+  o += 40 * spad > 8 * gb ? 40 * spad : 8 * gb;  // cost, id, tidx, pool, ord, rank, org, flag
   o = (int)align_up(o, 16);
   L.kk = o;
   if (method == MUX_KK) o += (int)sizeof(KkSmem);
@@ -859,6 +909,8 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
   int32_t* l_pool = l_tidx + spad;
   int32_t* l_ord = l_pool + spad;
   int32_t* l_rank = l_ord + spad;
+  int32_t* l_org = l_rank + spad;
+  int32_t* l_flag = l_org + spad;
   if (tid < kMaxKeys) s_carry[tid] = 0;
   __syncthreads();
   for (int base = 0; base < S; base += nt) {  // position of each encoder item in its pool
@@ -888,6 +940,7 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
       l_id[v] = w.id[i];
       l_tidx[v] = i;
       l_pool[v] = v < m0 ? 0 : 1;
+      l_org[v] = w.org[i];
     }
     l_ord[v] = v;
   }
@@ -895,11 +948,17 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
   if (m > 0) {
     if (W == 1) {
       for (int v = tid; v < m; v += nt) l_rank[v] = 0;
-    } else if (cfg.method == MUX_LPT) {
+    } else if (cfg.method == MUX_LPT || cfg.method == MUX_LPT_LOCAL) {
       bitonic_sort(l_ord, next_pow2(m), PoolKey{l_pool, l_cost, l_id, l_tidx, m});
       const int warp = tid >> 5;
-      if (warp == 0 && m0 > 0) lpt_warp(l_ord, l_cost, m0, W, l_rank);
-      if (warp == 1 && m1 > 0) lpt_warp(l_ord + m0, l_cost, m1, W, l_rank);
+      if (cfg.method == MUX_LPT) {
+        if (warp == 0 && m0 > 0) lpt_warp(l_ord, l_cost, m0, W, l_rank);
+        if (warp == 1 && m1 > 0) lpt_warp(l_ord + m0, l_cost, m1, W, l_rank);
+      } else {
+        if (warp == 0 && m0 > 0) lpt_local_warp(l_ord, l_cost, l_org, m0, W, l_rank, l_flag);
+        if (warp == 1 && m1 > 0)
+          lpt_local_warp(l_ord + m0, l_cost, l_org, m1, W, l_rank, l_flag + m0);
+      }
     } else if (m0 > kKkMax || m1 > kKkMax) {
       if (tid == 0) p.hdr[MUX_H_ERR_INDEX] = -2;  // KK pool limit
     } else {
@@ -1325,6 +1384,11 @@ extern "C" int mux_assign(int32_t method, const double* w, const int64_t* ids, i
   }
   if (g < 1 || g > 8) {
     set_error("group count %d outside 1..8", g);
+    return MUX_ERR_VALUE;
+  }
+  if (method != MUX_LPT && method != MUX_KK) {
+    set_error("stand-alone partition method must be LPT or KK (locality-first LPT needs "
+              "origins: use the step planner)");
     return MUX_ERR_VALUE;
   }
   if (n < 0 || n > 4096 || (method == MUX_KK && n > kKkMax)) {

@@ -72,7 +72,7 @@ def main():
             seen[s[0]] = s[1]
         t = oplan.step_table(list(carry or []) if cfg["carry"] else [], drawn, chunks, seen)
         carry = rest
-        for method in (("lpt",) if proj else ("lpt", "kk")):
+        for method in (("lpt_local",) if proj else ("lpt", "kk", "lpt_local")):
             path.method = method
             o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
             arenas = [[payload(int(o["arena_rows"][r, g]), d_in[g], 1000 * step + 10 * r + g)

@@ -195,3 +195,23 @@ def test_reshard_invariants_on_golden_batches():
             n_sharded = sum(len(v) > 1 for v in smap.values())
             assert prev is None or n_sharded <= prev
             prev = n_sharded
+
+
+def test_lpt_local_balances_like_lpt_and_moves_less():
+    # locality-first LPT: kept loads never exceed the balanced load; across the
+    # golden multi-rank steps it moves far fewer tokens for a similar max load
+    moved = {"lpt": 0, "lpt_local": 0}
+    worst = {"lpt": 0.0, "lpt_local": 0.0}
+    for name, st, t, _ in golden_steps():
+        if st["world"] < 2:
+            continue
+        for m in moved:
+            p = oracle_plan(t, st, m)
+            enc = p["enc"] >= 0
+            moved[m] += int(t["lens"][enc & (p["enc"] != p["origin"])].sum())
+            loads = p["recv_rows"].sum(1).astype(float)
+            worst[m] = max(worst[m], loads.max() / loads.mean())
+    assert moved["lpt_local"] < 0.7 * moved["lpt"]
+    assert worst["lpt_local"] <= worst["lpt"] * 1.1
+    r = oplan.lpt_local_assign([5.0, 5.0, 5.0, 5.0], [0, 1, 2, 3], [0, 0, 0, 1], 2)
+    assert r == [0, 0, 1, 1]  # rank 0 keeps what fits in T=10, the rest moves
