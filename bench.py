@@ -412,12 +412,11 @@ def run_ours(args):
         e2e = run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, world)
 
     # per step: fused planner (1) + dispatch copy (1, + flag wait at N>1) + return:
-    # projector: row-map + GEMM per projected group (+ signal + wait at N>1);
+    # projector: row map (side stream) + one grouped GEMM (+ signal + wait at N>1);
     # otherwise one return copy (+ flag wait at N>1)
     launches = 1 + 1 + (1 if world > 1 else 0)
     if projector:
-        launches += 2 * sum(1 for g in (0, 1) if path.weight[g] is not None)
-        launches += 2 if world > 1 else 0
+        launches += 2 + (2 if world > 1 else 0)
     else:
         launches += 1 + (1 if world > 1 else 0)
     line = {

@@ -218,7 +218,9 @@ int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, const int64_t
                         uint16_t* out, void* stream);
 
 /* Expand return pieces of rank `me`, group `group` into a per-row
- * destination table: row_dst[src_row] = (dst_rank << 40) | dst_row. */
+ * destination table: row_dst[src_row] = (dst_rank << 40) | dst_row.
+ * group = -1: every group in one launch, group g's table at
+ * row_dst + g * n_rows. */
 int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_t group,
                     int64_t* row_dst, int64_t n_rows, void* stream);
 
@@ -251,6 +253,22 @@ int mux_proj_scatter_dev(const uint16_t* X, const uint16_t* W, const uint16_t* b
                          int64_t M_max, const int64_t* M_dev, int32_t K, int32_t N,
                          const int64_t* row_dst, void* const* out_bases, int32_t num_sms,
                          void* stream);
+
+/* One projector problem of a grouped launch (one per encoder group). */
+typedef struct {
+  const uint16_t* X;       /* bf16 [M_max, K] encoder rows                     */
+  const uint16_t* W;       /* bf16 [N, K] nn.Linear weight                     */
+  const uint16_t* bias;    /* bf16 [N] or NULL                                 */
+  int64_t M_max;           /* rows X can hold; 0 drops the group               */
+  const int64_t* M_dev;    /* device row count (clamped to M_max) or NULL      */
+  int32_t K, reserved;
+  const int64_t* row_dst;  /* int64 [M_max]: (rank << 40) | row                */
+} mux_proj_group;
+
+/* Every group's projector + scatter in ONE persistent launch (tiles of group
+ * 0, then group 1, ...), sharing N and out_bases.  n_groups <= 2. */
+int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_groups, int32_t N,
+                             void* const* out_bases, int32_t num_sms, void* stream);
 
 #ifdef __cplusplus
 }

@@ -49,6 +49,13 @@ class PlanLayout(C.Structure):
     _fields_ = [(n, C.c_int64) for n in LAYOUT_FIELDS]
 
 
+class ProjGroup(C.Structure):
+    """mux_proj_group: one problem of a grouped projector launch."""
+    _fields_ = [("X", C.c_void_p), ("W", C.c_void_p), ("bias", C.c_void_p),
+                ("M_max", C.c_int64), ("M_dev", C.c_void_p), ("K", C.c_int32),
+                ("reserved", C.c_int32), ("row_dst", C.c_void_p)]
+
+
 # (name, restype, argtypes) for every exported symbol of include/mux_b200.h
 _P = C.c_void_p
 _SIGS = [
@@ -78,6 +85,8 @@ _SIGS = [
                                    C.c_int32, _P]),
     ("mux_proj_scatter_dev", C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P,
                                        C.c_int32, _P]),
+    ("mux_proj_scatter_grouped", C.c_int, [C.POINTER(ProjGroup), C.c_int32, C.c_int32, _P,
+                                           C.c_int32, _P]),
 ]
 EXPORTS = tuple(n for n, _, _ in _SIGS)
 

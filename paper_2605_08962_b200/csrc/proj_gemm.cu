@@ -42,11 +42,40 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Up to kMaxGroups independent problems (one per encoder group) share N and
+// the output buffers; their tiles are enumerated group after group, so one
+// persistent launch covers the whole step.
+constexpr int kMaxGroups = 2;
+
+struct GroupParams {
+  CUtensorMap ta[kMaxGroups];  // X_g [M_max_g, K_g]
+  CUtensorMap tb[kMaxGroups];  // W_g [N, K_g]
+  const uint16_t* bias[kMaxGroups];
+  const int64_t* row_dst[kMaxGroups];
+  const int64_t* M_dev[kMaxGroups];
+  int64_t M_max[kMaxGroups];
+  int K[kMaxGroups];
+  int n_groups, N;
+  void* const* out_bases;
+};
+
+struct TileMap {
+  int64_t tiles[kMaxGroups + 1];  // first tile of each group, then the total
+  int64_t M[kMaxGroups];
+  int kblocks[kMaxGroups];
+};
+
+__device__ __forceinline__ void locate(const TileMap& tm, int n_groups, int num_n, int64_t tile,
+                                       int& g, int& m_blk, int& n_blk) {
+  g = 0;
+  while (g + 1 < n_groups && tile >= tm.tiles[g + 1]) ++g;
+  const int64_t t = tile - tm.tiles[g];
+  m_blk = (int)(t / num_n);
+  n_blk = (int)(t % num_n);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
-    proj_scatter_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const uint16_t* __restrict__ bias,
-                        int64_t M_max, const int64_t* __restrict__ M_dev, int K, int N,
-                        const int64_t* __restrict__ row_dst, void* const* __restrict__ out_bases) {
+    proj_scatter_kernel(const __grid_constant__ GroupParams P) {
   using namespace umma;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -58,18 +87,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t M = M_max;
-  if (M_dev) {
-    const int64_t m = *M_dev;
-    M = m < M_max ? m : M_max;
+  const int N = P.N, num_n = N / BN, G = P.n_groups;
+  TileMap tm;
+  tm.tiles[0] = 0;
+  for (int g = 0; g < G; ++g) {
+    int64_t M = P.M_max[g];
+    if (P.M_dev[g]) {
+      const int64_t m = *P.M_dev[g];
+      M = m < M ? (m > 0 ? m : 0) : M;
+    }
+    tm.M[g] = M;
+    tm.kblocks[g] = P.K[g] / BK;
+    tm.tiles[g + 1] = tm.tiles[g] + ((M + BM - 1) / BM) * num_n;
   }
-  const int num_n = N / BN;
-  const int64_t num_tiles = ((M + BM - 1) / BM) * num_n;
-  const int kblocks = K / BK;
+  const int64_t num_tiles = tm.tiles[G];
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
+    for (int g = 0; g < G; ++g) {
+      tma_prefetch(&P.ta[g]);
+      tma_prefetch(&P.tb[g]);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -94,13 +131,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_blk = (int)(tile / num_n), n_blk = (int)(tile % num_n);
-        for (int kb = 0; kb < kblocks; ++kb) {
+        int g, m_blk, n_blk;
+        locate(tm, G, num_n, tile, g, m_blk, n_blk);
+        const CUtensorMap* ta = &P.ta[g];
+        const CUtensorMap* tb = &P.tb[g];
+        for (int kb = 0; kb < tm.kblocks[g]; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * BK, m_blk * BM, pol_a);
-          tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN, pol_b);
+          tma_load_2d(sa, ta, &full[stage], kb * BK, m_blk * BM, pol_a);
+          tma_load_2d(sa + A_BYTES, tb, &full[stage], kb * BK, n_blk * BN, pol_b);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -114,10 +154,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int g, m_blk, n_blk;
+        locate(tm, G, num_n, tile, g, m_blk, n_blk);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < tm.kblocks[g]; ++kb) {
           mbar_wait(&full[stage], phase);
           fence_after();
           const uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -151,12 +193,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m_blk = (int)(tile / num_n), n_blk = (int)(tile % num_n);
+      int g, m_blk, n_blk;
+      locate(tm, G, num_n, tile, g, m_blk, n_blk);
+      const uint16_t* bias = P.bias[g];
       const int64_t m = (int64_t)m_blk * BM + quarter * 32 + lane;
       char* my_dst = nullptr;
-      if (m < M) {
-        const int64_t rd = row_dst[m];
-        my_dst = static_cast<char*>(out_bases[rd >> 40]) +
+      if (m < tm.M[g]) {
+        const int64_t rd = P.row_dst[g][m];
+        my_dst = static_cast<char*>(P.out_bases[rd >> 40]) +
                  ((rd & kRowMask) * N + (int64_t)n_blk * BN + colgrp * 128) * 2;
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -266,18 +310,45 @@ extern "C" int mux_proj_scatter_dev(const uint16_t* X, const uint16_t* W, const 
                                     int64_t M_max, const int64_t* M_dev, int32_t K, int32_t N,
                                     const int64_t* row_dst, void* const* out_bases,
                                     int32_t num_sms, void* stream) {
+  mux_proj_group g{X, W, bias, M_max, M_dev, K, 0, row_dst};
+  return mux_proj_scatter_grouped(&g, 1, N, out_bases, num_sms, stream);
+}
+
+extern "C" int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_groups,
+                                        int32_t N, void* const* out_bases, int32_t num_sms,
+                                        void* stream) {
   using namespace proj;
-  if (K % BK || N % BN || K <= 0 || N <= 0 || M_max < 0) {
-    set_error("projector shape M=%lld K=%d N=%d: need K %% %d == 0 and N %% %d == 0",
-              (long long)M_max, K, N, BK, BN);
+  if (n_groups < 0 || n_groups > kMaxGroups || N <= 0 || N % BN) {
+    set_error("projector: %d groups (max %d), N=%d (need N %% %d == 0)", n_groups, kMaxGroups,
+              N, BN);
     return MUX_ERR_VALUE;
   }
-  if (M_max == 0) return MUX_OK;
-  CUtensorMap ta, tb;
-  int st = make_map(&ta, X, M_max, K, BM);
-  if (st) return st;
-  st = make_map(&tb, W, N, K, BN);
-  if (st) return st;
+  GroupParams P;
+  memset(&P, 0, sizeof(P));
+  P.N = N;
+  P.out_bases = out_bases;
+  int64_t tiles = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    const mux_proj_group& q = groups[i];
+    if (q.K % BK || q.K <= 0 || q.M_max < 0) {
+      set_error("projector shape M=%lld K=%d N=%d: need K %% %d == 0 and N %% %d == 0",
+                (long long)q.M_max, q.K, N, BK, BN);
+      return MUX_ERR_VALUE;
+    }
+    if (q.M_max == 0) continue;  // nothing to read: drop the group
+    const int g = P.n_groups++;
+    int st = make_map(&P.ta[g], q.X, q.M_max, q.K, BM);
+    if (st) return st;
+    st = make_map(&P.tb[g], q.W, N, q.K, BN);
+    if (st) return st;
+    P.bias[g] = q.bias;
+    P.row_dst[g] = q.row_dst;
+    P.M_dev[g] = q.M_dev;
+    P.M_max[g] = q.M_max;
+    P.K[g] = q.K;
+    tiles += ((q.M_max + BM - 1) / BM) * (N / BN);
+  }
+  if (P.n_groups == 0) return MUX_OK;
   static bool attr = false;
   if (!attr) {
     MUX_CUDA(cudaFuncSetAttribute(proj_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -290,10 +361,8 @@ extern "C" int mux_proj_scatter_dev(const uint16_t* X, const uint16_t* W, const 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t tiles = ((M_max + BM - 1) / BM) * (N / BN);
   const int grid = (int)(tiles < sms ? tiles : sms);
-  proj_scatter_kernel<<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(
-      ta, tb, bias, M_max, M_dev, K, N, row_dst, out_bases);
+  proj_scatter_kernel<<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(P);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

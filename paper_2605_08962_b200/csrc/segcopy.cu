@@ -291,13 +291,15 @@ __global__ void return_rows_kernel(Plan p, int group, int64_t* row_dst, int64_t 
                                    int stage_slot) {
   const int64_t npieces = p.hdr[MUX_H_N_RETURN];
   for (int64_t s = blockIdx.x; s < npieces; s += gridDim.x) {
-    if (p.rgroup[s] != group) continue;
+    if (group >= 0 && p.rgroup[s] != group) continue;
+    // group < 0: every group, group g's map at row_dst + g * n_rows
+    int64_t* rd = group >= 0 ? row_dst : row_dst + (int64_t)p.rgroup[s] * n_rows;
     const int64_t src = p.rsrc[s], dst = p.rdst[s], n = p.rrows[s];
     const bool staged = stage_slot >= 0 && p.rrank[s] != me;
     const int64_t tag = (int64_t)(staged ? stage_slot : p.rrank[s]) << 40;
     const int64_t base = staged ? src : dst;
     for (int64_t t = threadIdx.x; t < n; t += blockDim.x)
-      if (src + t < n_rows) row_dst[src + t] = tag | (base + t);
+      if (src + t < n_rows) rd[src + t] = tag | (base + t);
   }
 }
 

@@ -142,7 +142,8 @@ class MuxPath:
         if projector:
             self.weight = [None] * N_GROUPS
             self.bias = [None] * N_GROUPS
-            self.row_dst = torch.empty(rows, dtype=torch.int64, device=dev)
+            self.row_dst = torch.empty(N_GROUPS * rows, dtype=torch.int64, device=dev)
+            self._row_ring = [None] * self.RING
 
     # ------------------------------------------------------------------ setup
     def set_projector(self, group: int, weight: torch.Tensor, bias: torch.Tensor | None = None):
@@ -212,16 +213,26 @@ class MuxPath:
         if after is not None:
             side.wait_event(after)
         cfg = self.cfg_for(dtab.table)
-        self._ring[slot] = plan_step(dtab, cfg, self._ring[slot], side)
+        p = self._ring[slot] = plan_step(dtab, cfg, self._ring[slot], side)
+        if self.projector and not self.staged:
+            # the GEMM's row map depends only on the plan: build it here, off the
+            # step's critical path
+            if self._row_ring[slot] is None:
+                self._row_ring[slot] = torch.empty_like(self.row_dst)
+            self._row_map(p, self._row_ring[slot], side)
         self._ready[slot].record(side)
-        return self._ring[slot]
+        return p
 
-    def run_planned(self, slot: int, arenas, stream=None) -> Plan:
-        """Dispatch + return of the plan in ring `slot` on the main stream."""
+    def run_planned(self, slot: int, arenas, stream=None, encoder=None) -> Plan:
+        """Dispatch + return of the plan in ring `slot` on the main stream.
+        `encoder(plan, stream)`, if given, runs between them (the encoder
+        forward: receive windows in, `enc_out` rows out)."""
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         main.wait_event(self._ready[slot])
         p = self._ring[slot]
         self.dispatch(p, arenas, main)
+        if encoder is not None:
+            encoder(p, main)
         self._freed[slot] = self.return_scatter(p, main)
         return p
 
@@ -283,24 +294,38 @@ class MuxPath:
         ev.record(main)
         return ev
 
+    def _row_map(self, plan: Plan, row_dst: torch.Tensor, stream):
+        """row_dst[g * max_rows + m] = (rank << 40) | row of encoder row m of group g."""
+        _lib.check(_lib.lib().mux_return_rows(C.byref(plan.cfg), plan.ptr, -1,
+                                              row_dst.data_ptr(), self.max_rows,
+                                              _stream_ptr(stream)), "mux_return_rows")
+        plan.row_map = row_dst
+
     def _project(self, plan: Plan, main):
-        """GEMM on this (encoder) rank; the epilogue stores every row at its
-        (rank, row), on this GPU or an NVLink peer."""
+        """GEMM on this (encoder) rank, every group in one launch; the epilogue
+        stores every row at its (rank, row), on this GPU or an NVLink peer."""
         L = _lib.lib()
         s = _stream_ptr(main)
         hdr = plan.ptr + plan.layout.header
+        rmap = getattr(plan, "row_map", None)
+        if rmap is None:
+            self._row_map(plan, self.row_dst, main)
+            rmap = self.row_dst
+        groups = (_lib.ProjGroup * N_GROUPS)()
+        n = 0
         for g in range(N_GROUPS):
             if self.weight[g] is None:
                 continue
-            _lib.check(L.mux_return_rows(C.byref(plan.cfg), plan.ptr, g, self.row_dst.data_ptr(),
-                                         self.max_rows, s), "mux_return_rows")
             b = self.bias[g]
-            _lib.check(L.mux_proj_scatter_dev(
+            groups[n] = _lib.ProjGroup(
                 self.enc_out[g].data_ptr(), self.weight[g].data_ptr(),
                 0 if b is None else b.data_ptr(), self.max_rows,
-                hdr + 8 * (_lib.H_RECV_ROWS0 + g), self.d_enc[g], self.d_llm,
-                self.row_dst.data_ptr(), self.llm_dst[0].data_ptr(), self.gemm_ctas, s),
-                "mux_proj_scatter_dev")
+                hdr + 8 * (_lib.H_RECV_ROWS0 + g), self.d_enc[g], 0,
+                rmap.data_ptr() + 8 * g * self.max_rows)
+            n += 1
+        plan.row_map = None  # consumed; the next plan in this slot rebuilds it
+        _lib.check(L.mux_proj_scatter_grouped(groups, n, self.d_llm, self.llm_dst[0].data_ptr(),
+                                              self.gemm_ctas, s), "mux_proj_scatter_grouped")
         if self.world > 1:
             _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(),
                                     self.epoch_ctr.data_ptr(), s), "mux_signal")

@@ -225,8 +225,17 @@ class Plan:
 
 def plan_step(dtab: DeviceTable, cfg: PlanCfg, plan: Plan | None = None, stream=None) -> Plan:
     """Launch the device planner (stream-ordered, no host sync)."""
-    if plan is None or plan.layout.total < layout_of(cfg).total:
-        plan = Plan(cfg, dtab.blob.device)
+    if plan is None or plan.blob.numel() < layout_of(cfg).total:
+        old = plan
+        # zero-fill on the launching stream (the ticket must read 0), with headroom
+        # so a ring slot is not re-allocated every time the step grows
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+            need = layout_of(cfg).total
+            blob = torch.zeros(need + need // 2 if old is not None else need,
+                               dtype=torch.uint8, device=dtab.blob.device)
+            plan = Plan(cfg, dtab.blob.device, blob)
+        if old is not None:  # other streams may still read the old blob
+            old.blob.record_stream(torch.cuda.current_stream())
     else:
         plan.cfg = cfg
         plan.layout = layout_of(cfg)

@@ -69,13 +69,57 @@ def test_proj_scatter_device_count(cuda_device):
     assert bool((out[517:] == 0).all())
 
 
+def test_proj_grouped_two_encoders(cuda_device):
+    """Both encoder groups in one launch: different K, device row counts, rows
+    of both groups interleaved in one output; an empty group is skipped."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    N, R = 512, 3000
+    Ks, Mmax, Mdev = (1280, 512), (900, 600), (700, 333)
+    Xs = [torch.randn(Mmax[k], Ks[k], device="cuda", generator=g).to(torch.bfloat16)
+          for k in range(2)]
+    Ws = [(torch.randn(N, Ks[k], device="cuda", generator=g) / Ks[k] ** 0.5).to(torch.bfloat16)
+          for k in range(2)]
+    b1 = torch.randn(N, device="cuda", generator=g).to(torch.bfloat16)
+    perm = torch.randperm(R, generator=torch.Generator().manual_seed(2))
+    rd = [perm[:Mmax[0]].to(torch.int64).cuda(), perm[1000:1000 + Mmax[1]].to(torch.int64).cuda()]
+    mdev = torch.tensor(Mdev, dtype=torch.int64, device="cuda")
+    out = torch.zeros(R, N, dtype=torch.bfloat16, device="cuda")
+    bases = torch.tensor([out.data_ptr()], dtype=torch.int64, device="cuda")
+    groups = (_lib.ProjGroup * 2)(
+        _lib.ProjGroup(Xs[0].data_ptr(), Ws[0].data_ptr(), None, Mmax[0], mdev.data_ptr(),
+                       Ks[0], 0, rd[0].data_ptr()),
+        _lib.ProjGroup(Xs[1].data_ptr(), Ws[1].data_ptr(), b1.data_ptr(), Mmax[1],
+                       mdev.data_ptr() + 8, Ks[1], 0, rd[1].data_ptr()))
+    _lib.check(_lib.lib().mux_proj_scatter_grouped(groups, 2, N, bases.data_ptr(), 0,
+                                                   torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    written = torch.zeros(R, dtype=torch.bool, device="cuda")
+    for k in range(2):
+        m = Mdev[k]
+        ref = Xs[k][:m].float() @ Ws[k].float().t() + (b1.float() if k else 0.0)
+        got = out[rd[k][:m]].float()
+        assert bool(((got - ref).abs() <= RTOL * ref.abs() + ATOL).all()), f"group {k}"
+        written[rd[k][:m]] = True
+    assert bool((out[~written] == 0).all()), "rows past *M_dev were stored"
+    # an empty group (device count 0) and a dropped one (M_max 0) launch nothing wrong
+    out.zero_()
+    mdev[0] = 0
+    groups[1].M_max = 0
+    _lib.check(_lib.lib().mux_proj_scatter_grouped(groups, 2, N, bases.data_ptr(), 0,
+                                                   torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert bool((out == 0).all())
+
+
 def test_proj_rejects_bad_shapes(cuda_device):
     with pytest.raises(ValueError):
         _lib.check(_lib.lib().mux_proj_scatter(None, None, None, 10, 100, 256, None, None, 0, None))
 
 
-def test_cfg2_step_with_projector_matches_oracle(cuda_device):
-    """Full cfg2 step (ViT-600M -> 7B shapes): plan, pack, stand-in, projector+scatter."""
+@pytest.mark.parametrize("name,step", [("cfg2", 1), ("target1", 1)])
+def test_step_with_projector_matches_oracle(cuda_device, name, step):
+    """Full step at ViT-600M -> 7B shapes: plan, pack, stand-in, projector+scatter
+    (target1 step 1 has vision and audio rows: both groups in one GEMM launch)."""
     from oracle import dataplane as odp
     from oracle import planner as oplan
     from paper_2605_08962_b200 import configs, planner
@@ -83,14 +127,15 @@ def test_cfg2_step_with_projector_matches_oracle(cuda_device):
     from tests.helpers import golden_steps
     from tests.test_gpu_planner import to_table
 
-    for name, st, t, _ in golden_steps():
-        if name != "cfg2" or st["step"] != 1:
+    for nm, st, t, _ in golden_steps():
+        if nm != name or st["step"] != step or st["world"] != 1:
             continue
         cap, gbs = configs.CAPACITY, st["gbs"]
         d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, configs.D_LLM
         o = oplan.plan_step(t, cap, gbs, 1, 1, 1)
         path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_enc=d_enc, d_llm=d_llm,
                        projector=True)
+        assert name != "target1" or int(o["recv_rows"][0, 1]) > 0
         g = torch.Generator().manual_seed(3)
         Ws = [(torch.randn(d_llm, d_enc[k], generator=g) / d_enc[k] ** 0.5).to(torch.bfloat16)
               for k in range(2)]
@@ -124,4 +169,54 @@ def test_cfg2_step_with_projector_matches_oracle(cuda_device):
             mask[dst_row:dst_row + rows] = True
         assert bool((got[~mask] == 0).all())
         return
-    raise AssertionError("cfg2 golden step missing")
+    raise AssertionError(f"{name} golden step {step} missing")
+
+
+def test_pipelined_ring_matches_oracle(cuda_device):
+    """The bench's pipelined form: step k+1 planned on the side stream (plan ring,
+    row map built there) while step k moves; every step's LLM rows checked."""
+    from oracle import planner as oplan
+    from paper_2605_08962_b200 import configs, planner
+    from paper_2605_08962_b200.dataplane import MuxPath
+    from tests.helpers import golden_steps
+    from tests.test_gpu_planner import to_table
+
+    steps = [(st, t) for nm, st, t, _ in golden_steps() if nm == "target1" and st["world"] == 1]
+    steps = (steps * 3)[:6]  # more steps than ring slots
+    cap, gbs = configs.CAPACITY, steps[0][0]["gbs"]
+    d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, 512
+    path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_enc=d_enc, d_llm=d_llm,
+                   projector=True, method="lpt_local")
+    g = torch.Generator().manual_seed(5)
+    Ws = [(torch.randn(d_llm, d_enc[k], generator=g) / d_enc[k] ** 0.5).to(torch.bfloat16).cuda()
+          for k in range(2)]
+    for k in range(2):
+        path.set_projector(k, Ws[k], None)
+    tabs = [planner.DeviceTable(to_table(t), "cuda") for _, t in steps]
+    os_ = [oplan.plan_step(t, cap, gbs, 1, 1, 1, 1, "lpt_local") for _, t in steps]
+    arenas = [[torch.zeros(max(int(o["arena_rows"][0, k]), 1), d_in[k], dtype=torch.bfloat16,
+                           device="cuda") for k in range(2)] for o in os_]
+    R = path.RING
+    outs = []
+    path.plan_ahead(tabs[0], 0)
+    for k in range(len(steps)):
+        if k + 1 < len(steps):
+            path.plan_ahead(tabs[k + 1], (k + 1) % R)
+        path.llm_view().zero_()
+        path.run_planned(k % R, arenas[k],
+                         encoder=lambda p, s, k=k: path.encode_standin(p, tabs[k], s))
+        n = int(os_[k]["llm_rows"][0])
+        outs.append(path.llm_view(n).float().clone())
+    torch.cuda.synchronize()
+    from oracle import dataplane as odp
+    for k, ((st, t), o) in enumerate(zip(steps, os_)):
+        n = int(o["llm_rows"][0])
+        ref = torch.zeros(n, d_llm, device="cuda")
+        for (i, src, dst_rank, dst_row, rows) in o["pieces"]:
+            q = int(o["group"][i])
+            x = torch.from_numpy(odp.standin(int(t["ids"][i]), int(t["lens"][i]), d_enc[q])
+                                 .view(np.int16)).view(torch.bfloat16).cuda()
+            off = src - int(o["enc_off"][i])
+            ref[dst_row:dst_row + rows] = x[off:off + rows].float() @ Ws[q].float().t()
+        err = (outs[k] - ref).abs()
+        assert bool((err <= RTOL * ref.abs() + ATOL).all()), f"step {k}"
