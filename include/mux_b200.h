@@ -270,6 +270,15 @@ typedef struct {
 int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_groups, int32_t N,
                              void* const* out_bases, int32_t num_sms, void* stream);
 
+/* Same, and the launch's last CTA then publishes the next epoch to every
+ * peer (mux_signal fused into the GEMM: every row store, local or NVLink,
+ * is fenced at system scope before the flag).  sync: a zeroed uint32 the
+ * kernel re-arms. */
+int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int32_t n_groups, int32_t N,
+                                    void* const* out_bases, int32_t num_sms, int32_t me,
+                                    int32_t world, uint64_t* const* flags_peers, uint32_t* sync,
+                                    uint64_t* epoch_ctr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

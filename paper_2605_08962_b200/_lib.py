@@ -87,6 +87,9 @@ _SIGS = [
                                        C.c_int32, _P]),
     ("mux_proj_scatter_grouped", C.c_int, [C.POINTER(ProjGroup), C.c_int32, C.c_int32, _P,
                                            C.c_int32, _P]),
+    ("mux_proj_scatter_grouped_signal", C.c_int, [C.POINTER(ProjGroup), C.c_int32, C.c_int32,
+                                                  _P, C.c_int32, C.c_int32, C.c_int32, _P, _P,
+                                                  _P, _P]),
 ]
 EXPORTS = tuple(n for n, _, _ in _SIGS)
 

@@ -57,20 +57,49 @@ struct GroupParams {
   int K[kMaxGroups];
   int n_groups, N;
   void* const* out_bases;
+  // completion signal (world > 0): the last CTA publishes epoch+1 to every
+  // peer's flag slot `me`, as mux_signal does, after every CTA's stores
+  uint64_t* const* flags_peers;
+  uint64_t* epoch_ctr;
+  uint32_t* ticket;  // zero before the first launch; re-armed by the last CTA
+  int me, world;
 };
 
 struct TileMap {
   int64_t tiles[kMaxGroups + 1];  // first tile of each group, then the total
   int64_t M[kMaxGroups];
   int kblocks[kMaxGroups];
+  int num_m[kMaxGroups], stride[kMaxGroups];
 };
+
+__device__ __forceinline__ int gcd_int(int a, int b) {
+  while (b) {
+    const int t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// Row blocks are visited in a golden-ratio stride order (a permutation of
+// 0..num_m-1).  Encoder rows are in origin-rank order, so the rows bound for
+// one NVLink peer form contiguous blocks; visiting them in order would leave
+// all remote stores to one stretch (the tail, on rank 0) with nothing to hide
+// behind.  Spread out, they overlap the MMAs of local blocks.  The N-tiles of
+// a row block stay adjacent, so the A tile is still shared through L2.
+__device__ __forceinline__ int block_stride(int num_m) {
+  if (num_m <= 2) return 1;
+  int s = (int)(num_m * 0.6180339887) | 1;
+  while (gcd_int(s, num_m) != 1) s += 2;
+  return s % num_m;
+}
 
 __device__ __forceinline__ void locate(const TileMap& tm, int n_groups, int num_n, int64_t tile,
                                        int& g, int& m_blk, int& n_blk) {
   g = 0;
   while (g + 1 < n_groups && tile >= tm.tiles[g + 1]) ++g;
   const int64_t t = tile - tm.tiles[g];
-  m_blk = (int)(t / num_n);
+  m_blk = (int)(((t / num_n) * tm.stride[g]) % tm.num_m[g]);
   n_blk = (int)(t % num_n);
 }
 
@@ -98,7 +127,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tm.M[g] = M;
     tm.kblocks[g] = P.K[g] / BK;
-    tm.tiles[g + 1] = tm.tiles[g] + ((M + BM - 1) / BM) * num_n;
+    tm.num_m[g] = (int)((M + BM - 1) / BM);
+    tm.stride[g] = block_stride(tm.num_m[g]);
+    tm.tiles[g + 1] = tm.tiles[g] + (int64_t)tm.num_m[g] * num_n;
   }
   const int64_t num_tiles = tm.tiles[G];
 
@@ -251,9 +282,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   fence_before();
+  if (P.world > 0) __threadfence_system();  // this thread's (peer) row stores first
   __syncthreads();
   fence_after();
   if (warp == 1) tmem_free<512>(tmem_base);
+  if (P.world > 0 && warp == 0) {
+    __shared__ bool s_last;
+    if (lane == 0) s_last = atomicAdd(P.ticket, 1u) == gridDim.x - 1;
+    __syncwarp();
+    if (s_last) {
+      const uint64_t e = *P.epoch_ctr + 1;
+      __syncwarp();
+      if (lane == 0) {
+        *P.ticket = 0;
+        *P.epoch_ctr = e;
+      }
+      __threadfence_system();
+      if (lane < P.world) {
+        uint64_t* f = P.flags_peers[lane] + P.me;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+      }
+    }
+  }
 }
 
 // --- host: tensor maps through the driver entry point (no -lcuda link) --------
@@ -317,7 +367,20 @@ extern "C" int mux_proj_scatter_dev(const uint16_t* X, const uint16_t* W, const 
 extern "C" int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_groups,
                                         int32_t N, void* const* out_bases, int32_t num_sms,
                                         void* stream) {
+  return mux_proj_scatter_grouped_signal(groups, n_groups, N, out_bases, num_sms, 0, 0, nullptr,
+                                         nullptr, nullptr, stream);
+}
+
+extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int32_t n_groups,
+                                               int32_t N, void* const* out_bases, int32_t num_sms,
+                                               int32_t me, int32_t world,
+                                               uint64_t* const* flags_peers, uint32_t* sync,
+                                               uint64_t* epoch_ctr, void* stream) {
   using namespace proj;
+  if (world > 0 && (!flags_peers || !sync || !epoch_ctr || world > 32 || me < 0 || me >= world)) {
+    set_error("projector signal: need flags, sync and epoch pointers, 0 <= me < world <= 32");
+    return MUX_ERR_VALUE;
+  }
   if (n_groups < 0 || n_groups > kMaxGroups || N <= 0 || N % BN) {
     set_error("projector: %d groups (max %d), N=%d (need N %% %d == 0)", n_groups, kMaxGroups,
               N, BN);
@@ -348,7 +411,15 @@ extern "C" int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_
     P.K[g] = q.K;
     tiles += ((q.M_max + BM - 1) / BM) * (N / BN);
   }
-  if (P.n_groups == 0) return MUX_OK;
+  P.flags_peers = flags_peers;
+  P.epoch_ctr = epoch_ctr;
+  P.ticket = sync;
+  P.me = me;
+  P.world = world;
+  if (P.n_groups == 0) {
+    // nothing to compute: still publish the epoch (peers wait for it)
+    return world > 0 ? mux_signal(me, world, flags_peers, epoch_ctr, stream) : MUX_OK;
+  }
   static bool attr = false;
   if (!attr) {
     MUX_CUDA(cudaFuncSetAttribute(proj_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -114,7 +114,9 @@ class MuxPath:
         self.flags.tensor.zero_()
         self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
                         for g in range(N_GROUPS)]
-        self.sync = torch.zeros(6, dtype=torch.int32, device=dev)  # copy counters x3 tables
+        # copy counters x3 tables, then the projector's completion ticket
+        self.sync = torch.zeros(8, dtype=torch.int32, device=dev)
+        self.kernel_events = None  # (start, end) CUDA events around the return kernel
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
@@ -251,10 +253,16 @@ class MuxPath:
         peer and a flag wait orders the stream after every peer's copy."""
         L = _lib.lib()
         s = _stream_ptr(stream)
+        ke = self.kernel_events if which == 1 else None
+        if ke is not None:
+            ke[0].record(stream if stream is not None else torch.cuda.current_stream(self.device))
         if self.world == 1:
             _lib.check(L.mux_segcopy(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
                                      dst.data_ptr(), 0, self.sync[2 * which:].data_ptr(), s),
                        "mux_segcopy")
+            if ke is not None:
+                ke[1].record(stream if stream is not None else
+                             torch.cuda.current_stream(self.device))
             return
         # beside an overlapped projector (which holds shared memory) copy CTAs stay lean
         grid = -2 * self.num_sms if self.staged else 0
@@ -262,6 +270,8 @@ class MuxPath:
                                     dst.data_ptr(), grid, -1, self.flag_ptrs.data_ptr(),
                                     self.sync[2 * which:].data_ptr(), self.epoch_ctr.data_ptr(),
                                     s), "mux_segcopy_ex")
+        if ke is not None:
+            ke[1].record(stream if stream is not None else torch.cuda.current_stream(self.device))
         _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch_ctr.data_ptr(),
                               self.timeout_ms, self.wait_err.data_ptr(), s), "mux_wait")
 
@@ -324,11 +334,21 @@ class MuxPath:
                 rmap.data_ptr() + 8 * g * self.max_rows)
             n += 1
         plan.row_map = None  # consumed; the next plan in this slot rebuilds it
-        _lib.check(L.mux_proj_scatter_grouped(groups, n, self.d_llm, self.llm_dst[0].data_ptr(),
-                                              self.gemm_ctas, s), "mux_proj_scatter_grouped")
+        ke = self.kernel_events
+        if ke is not None:
+            ke[0].record(main)
+        if self.world == 1:
+            _lib.check(L.mux_proj_scatter_grouped(groups, n, self.d_llm,
+                                                  self.llm_dst[0].data_ptr(), self.gemm_ctas, s),
+                       "mux_proj_scatter_grouped")
+        else:  # the GEMM's last CTA signals every peer
+            _lib.check(L.mux_proj_scatter_grouped_signal(
+                groups, n, self.d_llm, self.llm_dst[0].data_ptr(), self.gemm_ctas, self.rank,
+                self.world, self.flag_ptrs.data_ptr(), self.sync[6:].data_ptr(),
+                self.epoch_ctr.data_ptr(), s), "mux_proj_scatter_grouped_signal")
+        if ke is not None:
+            ke[1].record(main)
         if self.world > 1:
-            _lib.check(L.mux_signal(self.rank, self.world, self.flag_ptrs.data_ptr(),
-                                    self.epoch_ctr.data_ptr(), s), "mux_signal")
             _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(),
                                   self.epoch_ctr.data_ptr(), self.timeout_ms,
                                   self.wait_err.data_ptr(), s), "mux_wait")

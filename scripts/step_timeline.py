@@ -38,7 +38,8 @@ def main():
     tables = bench.generate_steps(name, world, 4)
     path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
                    d_in=configs.D_IN, d_enc=configs.D_ENC, d_llm=configs.D_LLM,
-                   projector=proj, device=dev, group=group)
+                   projector=proj, device=dev, group=group,
+                   method=os.environ.get("MUX_METHOD", "lpt_local"))
     if proj:
         for g in range(2):
             path.set_projector(g, torch.randn(configs.D_LLM, configs.D_ENC[g], device=dev)
@@ -46,7 +47,9 @@ def main():
     dtabs = [DeviceTable(t, dev) for t in tables]
     arenas = []
     for d in dtabs:
-        info = path.plan(d).host()
+        pl = path.plan(d)
+        path.encode_standin(pl, d)  # realistic encoder rows (GEMM power is data-dependent)
+        info = pl.host()
         arenas.append([torch.randn(max(int(info["arena_rows"][rank, g]), 1), configs.D_IN[g],
                                    device=dev).to(torch.bfloat16) for g in range(2)])
     L = _lib.lib()
@@ -92,8 +95,27 @@ def main():
                            path.wait_err.data_ptr(), s)
                 marks.append(("return wait", ev()))
         elif world == 1 or path.ret_mode == _lib.RET_FINAL:
-            path.return_scatter(p, st)
-            marks.append(("return_rows + projector GEMM (+signal/wait)", ev()))
+            path._row_map(p, path.row_dst, st)
+            if os.environ.get("MUX_TIMELINE_LOCAL"):  # experiment: every store local
+                path.row_dst.bitwise_and_((1 << 40) - 1).bitwise_or_(rank << 40)
+            marks.append(("row map", ev()))
+            hdr = p.ptr + p.layout.header
+            groups = (_lib.ProjGroup * N_GROUPS)()
+            for g in range(N_GROUPS):
+                groups[g] = _lib.ProjGroup(path.enc_out[g].data_ptr(), path.weight[g].data_ptr(),
+                                           0, path.max_rows, hdr + 8 * (_lib.H_RECV_ROWS0 + g),
+                                           path.d_enc[g], 0,
+                                           path.row_dst.data_ptr() + 8 * g * path.max_rows)
+            L.mux_proj_scatter_grouped(groups, N_GROUPS, path.d_llm, path.llm_dst[0].data_ptr(),
+                                       int(os.environ.get("MUX_GEMM_CTAS", "0")), s)
+            marks.append(("projector GEMM", ev()))
+            if world > 1:
+                L.mux_signal(rank, world, path.flag_ptrs.data_ptr(), path.epoch_ctr.data_ptr(), s)
+                marks.append(("signal", ev()))
+                L.mux_wait(world, path.flags.tensor.data_ptr(), path.epoch_ctr.data_ptr(), 20000,
+                           path.wait_err.data_ptr(), s)
+                marks.append(("return wait", ev()))
+            p.row_map = None
         else:
             L.mux_segcopy_signal(C.byref(p.cfg), p.ptr, 1, path.enc_src.data_ptr(),
                                  path.stage_dst[0].data_ptr(), 0, path.flag_ptrs.data_ptr(),
@@ -118,8 +140,9 @@ def main():
             names = [m[0] for m in marks[1:]]
             acc.append([a[1].elapsed_time(b[1]) * 1e3 for a, b in zip(marks, marks[1:])])
     mean = np.mean(np.array(acc), axis=0).tolist()
+    rows = [[int(x) for x in path.plan(d).host()["recv_rows"][rank]] for d in dtabs]
     out = {"rank": rank, "world": world, "config": name,
-           "us": {n: round(v, 1) for n, v in zip(names, mean)}}
+           "us": {n: round(v, 1) for n, v in zip(names, mean)}, "recv_rows": rows}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
