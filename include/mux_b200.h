@@ -99,7 +99,13 @@ typedef struct {
   int32_t chunk_bytes;  /* copy work unit (0 = default 32 KiB)              */
   int32_t ret_mode;     /* MUX_RET_FINAL | MUX_RET_STAGED (sp == 1 only)      */
   int32_t row_bytes_grad[MUX_N_GROUPS]; /* gradient-return row bytes (0: = ret) */
+  /* LSSP eta split: lssp_sp = encoder Ulysses group size
+   * (1..MUX_LSSP_MAX, divides world; 0 = off); samples longer than lssp_eta
+   * are encoded in the SP state, one token shard per group member. */
+  int32_t lssp_sp, lssp_eta;
 } mux_plan_cfg;
+
+#define MUX_LSSP_MAX 8
 
 /* Byte offsets of every array inside the plan buffer (one device blob). */
 typedef struct {
@@ -130,6 +136,12 @@ typedef struct {
   int64_t gseg_src_row, gseg_dst_row, gseg_rows;    /* int64[S*(sp+1)]    */
   int64_t gseg_group, gseg_dst_rank;                /* int32[S*(sp+1)]    */
   int64_t gseg_chunk0;                              /* int64[S*(sp+1)+1]  */
+  /* LSSP (lssp_sp > 0): state per sample (0 DP, 1 SP, -1 not encoded) and
+   * encoder-buffer row per (sample, shard): DP in column 0 on the home rank,
+   * SP shard k on group member k.  With LSSP the dispatch table holds up to
+   * S*lssp_sp segments and the return/gradient tables S*(sp+1+lssp_sp). */
+  int64_t lssp_state;                               /* int32[S]           */
+  int64_t lssp_row;                                 /* int64[S*MUX_LSSP_MAX] */
   int64_t total;
 } mux_plan_layout;
 

@@ -32,7 +32,8 @@ class PlanCfg(C.Structure):
         "mbs", "method", "pooled", "me", "mode")] + [
         ("row_bytes_in", C.c_int32 * N_GROUPS), ("row_bytes_ret", C.c_int32 * N_GROUPS),
         ("chunk_bytes", C.c_int32), ("ret_mode", C.c_int32),
-        ("row_bytes_grad", C.c_int32 * N_GROUPS)]
+        ("row_bytes_grad", C.c_int32 * N_GROUPS), ("lssp_sp", C.c_int32),
+        ("lssp_eta", C.c_int32)]
 
 
 LAYOUT_FIELDS = (
@@ -42,7 +43,9 @@ LAYOUT_FIELDS = (
     "recv_rows", "stage_rows", "llm_rows", "order", "scratch_a", "scratch_b", "dseg_src_row", "dseg_dst_row",
     "dseg_rows", "dseg_group", "dseg_dst_rank", "dseg_chunk0", "rseg_src_row", "rseg_dst_row",
     "rseg_rows", "rseg_group", "rseg_dst_rank", "rseg_chunk0", "gseg_src_row", "gseg_dst_row",
-    "gseg_rows", "gseg_group", "gseg_dst_rank", "gseg_chunk0", "total")
+    "gseg_rows", "gseg_group", "gseg_dst_rank", "gseg_chunk0", "lssp_state", "lssp_row",
+    "total")
+LSSP_MAX = 8
 
 
 class PlanLayout(C.Structure):

@@ -121,14 +121,20 @@ struct Plan {
   int32_t *rgroup, *rrank;
   int64_t *gsrc, *gdst, *grows, *gchunk0;
   int32_t *ggroup, *grank;
+  int32_t* lssp_state;
+  int64_t* lssp_row;  // [S][MUX_LSSP_MAX]
 };
 
 Plan make_plan(void* base, const mux_plan_layout& L);
+// LSSP re-targeting of a step plan (lssp.cu), launched after plan_kernel.
+int launch_lssp(const mux_plan_cfg& cfg, const int32_t* lens, const Plan& p, cudaStream_t stream);
 Plan make_plan_const(const void* base, const mux_plan_layout& L);
 
 // Upper bounds used by the layout.
 inline int max_seq_of(const mux_plan_cfg& c) { return c.n_carry_seqs + (c.S - c.n_carry) + 1; }
-inline int max_ret_of(const mux_plan_cfg& c) { return c.S * (c.sp + 1) + 1; }
+inline int lssp_of(const mux_plan_cfg& c) { return c.lssp_sp > 0 ? c.lssp_sp : 0; }
+inline int max_ret_of(const mux_plan_cfg& c) { return c.S * (c.sp + 1 + lssp_of(c)) + 1; }
+inline int max_disp_of(const mux_plan_cfg& c) { return c.S * (lssp_of(c) > 1 ? lssp_of(c) : 1); }
 constexpr int kDefaultChunkBytes = 32768;
 
 }  // namespace mux

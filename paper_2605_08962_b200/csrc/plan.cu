@@ -62,6 +62,15 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
       set_error("staged projector return needs Ulysses sp == 1 (got %d)", c.sp);
       return MUX_ERR_VALUE;
     }
+    if (c.lssp_sp < 0 || c.lssp_sp > MUX_LSSP_MAX ||
+        (c.lssp_sp > 0 && (c.world % c.lssp_sp || c.ret_mode != MUX_RET_FINAL || c.lssp_eta < 0))) {
+      set_error("LSSP group %d: need 1..%d dividing world %d, eta >= 0, final-row return",
+                c.lssp_sp, MUX_LSSP_MAX, c.world);
+      return MUX_ERR_VALUE;
+    }
+  } else if (c.lssp_sp != 0) {
+    set_error("LSSP applies to step plans only");
+    return MUX_ERR_VALUE;
   }
   const int64_t S = c.S > 0 ? c.S : 1;
   const int64_t nch = c.n_chunks > 0 ? c.n_chunks : 1;
@@ -107,12 +116,13 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->order = take(4 * S);
   L->scratch_a = take(4 * S);
   L->scratch_b = take(4 * S);
-  L->dseg_src_row = take(8 * S);
-  L->dseg_dst_row = take(8 * S);
-  L->dseg_rows = take(8 * S);
-  L->dseg_group = take(4 * S);
-  L->dseg_dst_rank = take(4 * S);
-  L->dseg_chunk0 = take(8 * (S + 1));
+  const int64_t D = c.S > 0 ? max_disp_of(c) : 1;
+  L->dseg_src_row = take(8 * D);
+  L->dseg_dst_row = take(8 * D);
+  L->dseg_rows = take(8 * D);
+  L->dseg_group = take(4 * D);
+  L->dseg_dst_rank = take(4 * D);
+  L->dseg_chunk0 = take(8 * (D + 1));
   L->rseg_src_row = take(8 * R);
   L->rseg_dst_row = take(8 * R);
   L->rseg_rows = take(8 * R);
@@ -125,6 +135,8 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->gseg_group = take(4 * R);
   L->gseg_dst_rank = take(4 * R);
   L->gseg_chunk0 = take(8 * (R + 1));
+  L->lssp_state = take(4 * S);
+  L->lssp_row = take(8 * S * MUX_LSSP_MAX);
   L->total = o;
   return MUX_OK;
 }
@@ -186,6 +198,8 @@ Plan make_plan(void* b, const mux_plan_layout& L) {
   p.ggroup = at<int32_t>(b, L.gseg_group);
   p.grank = at<int32_t>(b, L.gseg_dst_rank);
   p.gchunk0 = at<int64_t>(b, L.gseg_chunk0);
+  p.lssp_state = at<int32_t>(b, L.lssp_state);
+  p.lssp_row = at<int64_t>(b, L.lssp_row);
   return p;
 }
 
@@ -1341,6 +1355,8 @@ extern "C" int mux_plan_step(const mux_plan_cfg* cfg, const int32_t* lens, const
   plan_kernel<<<grid, threads, smem, static_cast<cudaStream_t>(stream)>>>(
       *cfg, lens, mods, ids, carry_seq, chunk_off, p);
   MUX_CUDA(cudaGetLastError());
+  if (cfg->mode == MUX_MODE_STEP && cfg->lssp_sp > 0)
+    return launch_lssp(*cfg, lens, p, static_cast<cudaStream_t>(stream));
   return MUX_OK;
 }
 

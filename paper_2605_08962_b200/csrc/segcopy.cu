@@ -260,17 +260,38 @@ __device__ __forceinline__ uint32_t standin_bits(uint32_t row_seed, uint32_t c) 
 
 __global__ void __launch_bounds__(256) standin_kernel(Plan p, int S, int me, int group,
                                                      const int64_t* ids, const int32_t* lens,
-                                                     int width, uint16_t* out) {
+                                                     int width, uint16_t* out, int lssp_G) {
   for (int i = blockIdx.y; i < S; i += gridDim.y) {
-    if (p.enc[i] != me || p.group[i] != group) continue;
+    if (p.group[i] != group) continue;
+    // rows of sample i this rank encodes: tokens [t0, t0 + L) at rows r0..
+    int t0 = 0, L = lens[i];
+    int64_t r0;
+    if (lssp_G > 0) {  // LSSP: DP samples whole at home, SP shard k on member k
+      const int st = p.lssp_state[i], e = p.enc[i];
+      if (st == 0) {
+        if (e != me) continue;
+        r0 = p.lssp_row[(int64_t)i * MUX_LSSP_MAX];
+      } else if (st == 1) {
+        const int k = me - (e - e % lssp_G);
+        if (k < 0 || k >= lssp_G) continue;
+        const int b = L / lssp_G, rem = L % lssp_G;
+        t0 = k * b + (k < rem ? k : rem);
+        L = b + (k < rem ? 1 : 0);
+        r0 = p.lssp_row[(int64_t)i * MUX_LSSP_MAX + k];
+      } else {
+        continue;
+      }
+    } else {
+      if (p.enc[i] != me) continue;
+      r0 = p.enc_off[i];
+    }
     const int64_t id = ids[i];
     const uint32_t sseed = mix32((uint32_t)id ^ mix32((uint32_t)((uint64_t)id >> 32) + 0x632be59bu));
-    const int L = lens[i];
-    const int64_t r0 = p.enc_off[i];
     const int nv = width / 8;
-    for (int t = blockIdx.x; t < L; t += gridDim.x) {
+    for (int j = blockIdx.x; j < L; j += gridDim.x) {
+      const int t = t0 + j;
       const uint32_t rs = mix32(sseed + (uint32_t)t * 0x9e3779b9u);
-      uint4* row = reinterpret_cast<uint4*>(out + (r0 + t) * width);
+      uint4* row = reinterpret_cast<uint4*>(out + (r0 + j) * width);
       for (int v = threadIdx.x; v < nv; v += blockDim.x) {
         const uint32_t c = v * 8;
         uint4 w;
@@ -430,8 +451,8 @@ extern "C" int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, co
   if (st) return st;
   Plan p = make_plan_const(plan, L);
   dim3 grid(64, cfg->S > 0 ? (cfg->S < 1024 ? cfg->S : 1024) : 1);
-  standin_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, cfg->S, cfg->me, group,
-                                                                      ids, lens, width, out);
+  standin_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      p, cfg->S, cfg->me, group, ids, lens, width, out, cfg->lssp_sp);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

@@ -86,7 +86,8 @@ class MuxPath:
                  rank: int = 0, method: str = "lpt", pooled: bool = False,
                  d_in=(588, 512), d_enc=(1280, 1280), d_llm: int = 4096,
                  projector: bool = False, device=None, group=None, max_rows: int | None = None,
-                 wait_timeout_ms: int = 20000, projector_return: str | None = None):
+                 wait_timeout_ms: int = 20000, projector_return: str | None = None,
+                 lssp_eta: int | None = None, lssp_sp: int = 1):
         self.capacity, self.gbs, self.dp, self.sp = capacity, gbs, dp, sp
         self.world, self.rank, self.method, self.pooled = world, rank, method, pooled
         self.d_in, self.d_enc, self.d_llm = tuple(d_in), tuple(d_enc), d_llm
@@ -99,6 +100,11 @@ class MuxPath:
         if mode not in ("fused", "staged"):
             raise ValueError(f"projector_return must be 'fused' or 'staged', not {mode!r}")
         self.projector_return = mode
+        # LSSP eta split: samples longer than lssp_eta are encoded
+        # as token shards over groups of lssp_sp consecutive ranks (None: off)
+        if lssp_eta is not None and (lssp_sp < 1 or world % lssp_sp):
+            raise ValueError(f"lssp_sp {lssp_sp} must divide world {world}")
+        self.lssp_eta, self.lssp_sp = lssp_eta, lssp_sp
         self.staged = bool(projector and world > 1 and mode == "staged")
         self.ret_mode = _lib.RET_STAGED if self.staged else _lib.RET_FINAL
         rows = max_rows or gbs * capacity                       # all batch tokens
@@ -160,7 +166,9 @@ class MuxPath:
                         self.method, self.pooled, self.rank,
                         row_bytes_in=tuple(2 * d for d in self.d_in),
                         row_bytes_ret=tuple(2 * d for d in self.d_ret), ret_mode=self.ret_mode,
-                        row_bytes_grad=(2 * self.d_llm,) * N_GROUPS)
+                        row_bytes_grad=(2 * self.d_llm,) * N_GROUPS,
+                        lssp_sp=self.lssp_sp if self.lssp_eta is not None else 0,
+                        lssp_eta=self.lssp_eta or 0)
 
     @property
     def llm(self) -> _Window:

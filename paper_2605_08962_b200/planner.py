@@ -117,7 +117,11 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
              world: int = 1, mbs: int = 1, method: str = "lpt", pooled: bool = False,
              me: int = 0, mode: int = _lib.MODE_STEP, row_bytes_in=(1176, 1024),
              row_bytes_ret=(8192, 8192), chunk_bytes: int = DEFAULT_CHUNK_BYTES,
-             ret_mode: int = _lib.RET_FINAL, row_bytes_grad=None) -> PlanCfg:
+             ret_mode: int = _lib.RET_FINAL, row_bytes_grad=None, lssp_sp: int = 0,
+             lssp_eta: int = 0) -> PlanCfg:
+    """One step's planner configuration (include/mux_b200.h mux_plan_cfg).
+    lssp_sp > 0 turns on the LSSP eta split (samples longer than lssp_eta are
+    encoded as token shards over groups of lssp_sp ranks; oracle/lssp.py)."""
     if method not in METHODS:
         raise ValueError(f"unknown balance method {method!r}")
     c = PlanCfg()
@@ -132,6 +136,7 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
     c.ret_mode = ret_mode
     for g in range(_lib.N_GROUPS):
         c.row_bytes_grad[g] = 0 if row_bytes_grad is None else row_bytes_grad[g]
+    c.lssp_sp, c.lssp_eta = int(lssp_sp), int(lssp_eta)
     return c
 
 
@@ -147,9 +152,9 @@ class Plan:
     I32 = ("seq", "off", "span", "origin", "origin_pos", "group", "enc", "llm_rank",
            "bin_of", "fills", "nspans", "cu", "shard_len", "shard_start", "dseg_group",
            "dseg_dst_rank", "rseg_group", "rseg_dst_rank", "chunk_nbins", "gseg_group",
-           "gseg_dst_rank")
+           "gseg_dst_rank", "lssp_state")
     I64 = ("arena_off", "enc_off", "llm_row", "row_base", "arena_rows", "recv_rows", "llm_rows",
-           "dseg_src_row", "dseg_dst_row", "dseg_rows", "rseg_src_row", "rseg_dst_row",
+           "lssp_row", "dseg_src_row", "dseg_dst_row", "dseg_rows", "rseg_src_row", "rseg_dst_row",
            "rseg_rows", "dseg_chunk0", "rseg_chunk0", "gseg_src_row", "gseg_dst_row",
            "gseg_rows", "gseg_chunk0")
 
@@ -214,6 +219,10 @@ class Plan:
                                     self.view("dseg_group", nd).cpu().numpy().astype(np.int64),
                                     self.view("dseg_dst_rank", nd).cpu().numpy().astype(np.int64)],
                                    axis=1) if nd else np.zeros((0, 5), np.int64)
+            if c.lssp_sp > 0:
+                out["lssp_state"] = self.view("lssp_state", S).cpu().numpy()
+                out["lssp_row"] = self.view("lssp_row", S * _lib.LSSP_MAX).cpu().numpy() \
+                    .reshape(S, _lib.LSSP_MAX)[:, :c.lssp_sp]
             out["rseg"] = np.stack([self.view("rseg_src_row", nr).cpu().numpy(),
                                     self.view("rseg_dst_row", nr).cpu().numpy(),
                                     self.view("rseg_rows", nr).cpu().numpy(),

@@ -20,6 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import dataplane as odp  # noqa: E402
+from oracle import lssp as olssp  # noqa: E402
 from oracle import planner as oplan  # noqa: E402
 from oracle import workload as owork  # noqa: E402
 from paper_2605_08962_b200 import configs, planner  # noqa: E402
@@ -35,6 +36,7 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
     narrow = "narrow" in sys.argv
     proj = "proj" in sys.argv
+    lssp = "lssp" in sys.argv  # LSSP eta split: long samples sharded over encoder groups
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -55,7 +57,8 @@ def main():
     path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
                    d_in=d_in, d_enc=d_enc, d_llm=d_llm, device=dev, group=dist.group.WORLD,
                    projector=proj,
-                   projector_return="staged" if "staged" in sys.argv else "fused")
+                   projector_return="staged" if "staged" in sys.argv else "fused",
+                   lssp_eta=2048 if lssp else None, lssp_sp=world if lssp else 1)
     if proj:
         gw = torch.Generator().manual_seed(9)
         Ws = [(torch.randn(d_llm, d_enc[g], generator=gw) / d_enc[g] ** 0.5).to(torch.bfloat16)
@@ -75,6 +78,10 @@ def main():
         for method in (("lpt_local",) if proj else ("lpt", "kk", "lpt_local")):
             path.method = method
             o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
+            lay = None
+            if lssp:  # group of all ranks on even steps, pairs on odd steps
+                path.lssp_sp = world if step % 2 == 0 else 2
+                lay = olssp.layout(o, t["lens"], world, path.lssp_eta, path.lssp_sp)
             arenas = [[payload(int(o["arena_rows"][r, g]), d_in[g], 1000 * step + 10 * r + g)
                        for g in range(2)] for r in range(world)]
             table = planner.StepTable(t["lens"].astype(np.int32), t["mods"].astype(np.int32),
@@ -116,9 +123,14 @@ def main():
                     fails += 1
                 dist.barrier()
                 continue
-            recv, _, llm = odp.run_world(o, t, world, ar, d_in, (d_llm, d_llm), d_llm)
+            if lay is None:
+                recv, _, llm = odp.run_world(o, t, world, ar, d_in, (d_llm, d_llm), d_llm)
+                rows_of = o["recv_rows"]
+            else:
+                recv, _, llm = olssp.run_world(o, lay, t, world, ar, d_in, (d_llm, d_llm), d_llm)
+                rows_of = lay["recv_rows"]
             for g in range(2):
-                n = int(o["recv_rows"][rank, g])
+                n = int(rows_of[rank, g])
                 got = path.recv_view(g, n).cpu().view(torch.int16).numpy().view(np.uint16)
                 if not np.array_equal(got, recv[rank][g]):
                     print(f"rank {rank} step {step} {method}: recv group {g} differs", flush=True)
@@ -135,10 +147,11 @@ def main():
             path.grad_return(plan, dys[rank].to(dev))
             torch.cuda.synchronize()
             path.check_wait()
-            want = odp.run_grad(o, world, [d.view(torch.int16).numpy().view(np.uint16)
-                                           for d in dys], d_llm)
+            dyh = [d.view(torch.int16).numpy().view(np.uint16) for d in dys]
+            want = odp.run_grad(o, world, dyh, d_llm) if lay is None else \
+                olssp.run_grad(lay, world, dyh, d_llm)
             for g in range(2):
-                r_ = int(o["recv_rows"][rank, g])
+                r_ = int(rows_of[rank, g])
                 got = path.grad_view(g, r_).cpu().view(torch.int16).numpy().view(np.uint16)
                 if not np.array_equal(got, want[rank][g]):
                     print(f"rank {rank} step {step} {method}: gradient group {g} differs",

@@ -96,3 +96,52 @@ def test_standin_matches_oracle(cuda_device):
              ids=np.array([2 ** 40 + 5, 99_000_017, 3]), carry_seq=np.zeros(0, np.int64),
              n_carry_seqs=0, chunk_off=[0, 3])
     run_step(t, 16, 1, (8, 8), 24)
+
+
+@pytest.mark.parametrize("eta", [0, 3000])
+def test_dataplane_lssp_one_gpu(cuda_device, eta):
+    """LSSP on one GPU (group of 1): DP rows first, then the SP samples, each
+    buffer bit-exact against oracle/lssp.py; the packed LLM input is unchanged."""
+    from oracle import lssp as olssp
+    for name, st, t, _ in golden_steps():
+        if name != "target1" or st["world"] != 1 or st["step"] != 1:
+            continue
+        cap, gbs, d_in, d_llm = configs.CAPACITY, st["gbs"], (20, 8), 64
+        o = oplan.plan_step(t, cap, gbs, 1, 1, 1, 1, "lpt")
+        lay = olssp.layout(o, t["lens"], 1, eta, 1)
+        assert (lay["state"] == 1).any() and (eta == 0 or (lay["state"] == 0).any())
+        arenas_cpu = [payload(int(o["arena_rows"][0, g]), d_in[g], 100 + g) for g in range(2)]
+        path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_llm=d_llm, method="lpt",
+                       lssp_eta=eta, lssp_sp=1)
+        table = to_table(t)
+        dtab = planner.DeviceTable(table, "cuda")
+        plan = path.plan(dtab)
+        plan.check(table)
+        path.llm_view().zero_()
+        path.dispatch(plan, [a.cuda() for a in arenas_cpu])
+        path.encode_standin(plan, dtab)
+        path.return_scatter(plan)
+        torch.cuda.synchronize()
+        ar = [[a.view(torch.int16).numpy().view(np.uint16) for a in arenas_cpu]]
+        recv, enc_out, llm = olssp.run_world(o, lay, t, 1, ar, d_in, (d_llm, d_llm), d_llm)
+        for g in range(2):
+            n = int(lay["recv_rows"][0, g])
+            got = path.recv_view(g, n).cpu().view(torch.int16).numpy().view(np.uint16)
+            assert np.array_equal(got, recv[0][g]), f"recv group {g}"
+            got = path.enc_view(g, n).cpu().view(torch.int16).numpy().view(np.uint16)
+            assert np.array_equal(got, enc_out[0][g]), f"encoder rows group {g}"
+        n = int(o["llm_rows"][0])
+        got = path.llm_view(n).cpu().view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got, llm[0])
+        _, _, llm_plain = odp.run_world(o, t, 1, ar, d_in, (d_llm, d_llm), d_llm)
+        assert np.array_equal(got, llm_plain[0]), "LLM input must not depend on the split"
+        dy = payload(max(n, 1), d_llm, 7).cuda()
+        path.grad_return(plan, dy)
+        torch.cuda.synchronize()
+        want = olssp.run_grad(lay, 1, [dy.cpu().view(torch.int16).numpy().view(np.uint16)], d_llm)
+        for g in range(2):
+            r = int(lay["recv_rows"][0, g])
+            got = path.grad_view(g, r).cpu().view(torch.int16).numpy().view(np.uint16)
+            assert np.array_equal(got, want[0][g]), f"gradient group {g}"
+        return
+    raise AssertionError("target1 golden step missing")

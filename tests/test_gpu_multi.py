@@ -17,7 +17,8 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("config", ["cfg5", "cfg3", "cfg4", "cfg2 proj", "cfg2 proj staged"])
+@pytest.mark.parametrize("config", ["cfg5", "cfg3", "cfg4", "cfg2 proj", "cfg2 proj staged",
+                                    "cfg5 lssp"])
 def test_push_exchange_bit_exact(config):
     n = _ngpus()
     if n < 2:

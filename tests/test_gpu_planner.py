@@ -198,3 +198,82 @@ def test_grouped_reorder_and_restore(cuda_device):
         bad = balance.ReorderRecord(forward={(0, 0): (0, 0), (0, 1): (0, 0)}, shape=[2])
         balance.restore_order(bad, [[1, 2]])
     assert balance.zero_redundancy_filter(None, 1, 4, 16) == [1, 5, 9, 13]
+
+
+def lssp_device_plan(t, cap, gbs, dp, sp, world, me, method, sp_enc, eta):
+    table = to_table(t)
+    cfg = planner.make_cfg(table, cap, gbs, dp, sp, world, 1, method, False, me,
+                           row_bytes_in=(1176, 1024), row_bytes_ret=(8192, 8192),
+                           lssp_sp=sp_enc, lssp_eta=eta)
+    plan = planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
+    plan.check(table)
+    return plan.host()
+
+
+def assert_lssp_equal(d, o, lay, t, me):
+    from oracle import lssp as olssp
+    items = np.flatnonzero(o["enc"] >= 0)
+    assert np.array_equal(d["lssp_state"][items], lay["state"][items])
+    for i in items:
+        cols = 1 if lay["state"][i] == 0 else lay["sp_enc"]
+        assert np.array_equal(d["lssp_row"][i, :cols], lay["row"][i, :cols]), i
+    assert np.array_equal(d["recv_rows"], lay["recv_rows"])
+    assert np.array_equal(d["dseg"], olssp.dispatch_by_rank(o, lay, t["lens"], me))
+    assert np.array_equal(d["rseg"], olssp.return_by_rank(lay, me))
+    assert np.array_equal(d["gseg"], olssp.grad_by_rank(lay, me))
+    h = d["header"]
+    assert [int(h[12]), int(h[13])] == lay["recv_rows"][me].tolist()
+
+
+@pytest.mark.parametrize("sp_enc", [1, 2, 4, 8])
+def test_lssp_plan_matches_oracle_on_golden_steps(cuda_device, sp_enc):
+    from oracle import lssp as olssp
+    n = 0
+    for name, st, t, _ in golden_steps():
+        world, dp = st["world"], st["dp"]
+        if world % sp_enc:
+            continue
+        o = oracle_plan(t, st, "lpt_local")
+        lens = np.asarray(t["lens"])
+        items = np.flatnonzero(o["enc"] >= 0)
+        for eta in (0, int(np.median(lens[items])) if len(items) else 0, 4096):
+            lay = olssp.layout(o, lens, world, eta, sp_enc)
+            for me in range(world):
+                d = lssp_device_plan(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, me,
+                                     "lpt_local", sp_enc, eta)
+                assert_lssp_equal(d, o, lay, t, me)
+                n += 1
+    assert n > 10
+
+
+def test_lssp_plan_matches_oracle_random_tables(cuda_device):
+    from oracle import lssp as olssp
+    rs = np.random.RandomState(17)
+    checked = 0
+    for it in range(80):
+        t, cap = random_table(rs)
+        world, dp = [(2, 2), (4, 4), (4, 2), (8, 8), (8, 4), (2, 1)][it % 6]
+        sp_enc = int(rs.choice([g for g in (1, 2, 4, 8) if world % g == 0]))
+        sp = world // dp
+        gbs = dp * int(rs.randint(1, 3))
+        try:
+            o = oplan.plan_step(t, cap, gbs, dp, sp, world, 1, "lpt")
+        except ValueError:
+            continue
+        eta = int(rs.randint(0, cap + 1))
+        lay = olssp.layout(o, t["lens"], world, eta, sp_enc)
+        me = int(rs.randint(0, world))
+        d = lssp_device_plan(t, cap, gbs, dp, sp, world, me, "lpt", sp_enc, eta)
+        assert_lssp_equal(d, o, lay, t, me)
+        checked += 1
+    assert checked > 40
+
+
+def test_lssp_rejects_bad_groups(cuda_device):
+    t = golden_steps().__next__()[2]
+    table = to_table(t)
+    for sp_enc in (3, 9):
+        cfg = planner.make_cfg(table, configs.CAPACITY, 4, 4, 1, 4, 1, "lpt", False, 0,
+                               lssp_sp=sp_enc, lssp_eta=10)
+        with pytest.raises(ValueError, match="LSSP"):
+            planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)

@@ -215,3 +215,74 @@ def test_lpt_local_balances_like_lpt_and_moves_less():
     assert worst["lpt_local"] <= worst["lpt"] * 1.1
     r = oplan.lpt_local_assign([5.0, 5.0, 5.0, 5.0], [0, 1, 2, 3], [0, 0, 0, 1], 2)
     assert r == [0, 0, 1, 1]  # rank 0 keeps what fits in T=10, the rest moves
+
+
+# ---------------------------------------------------------------- LSSP eta split
+from oracle import dataplane as odp  # noqa: E402
+from oracle import lssp as olssp  # noqa: E402
+
+
+def _one_seq_table(lens, mod=1):
+    n = len(lens)
+    return dict(lens=np.array(lens, np.int64), mods=np.full(n, mod, np.int64),
+                ids=np.arange(100, 100 + n, dtype=np.int64), carry_seq=np.zeros(0, np.int64),
+                n_carry_seqs=0, chunk_off=[0, n])
+
+
+def test_lssp_spec_kat_threshold_split():
+    """SPEC.md lssp_schedule example: lengths [1024, 2048, 9000, 512], eta=4096
+    -> DP {1024, 2048, 512}, SP {9000}; eta = max length -> pure DP."""
+    t = _one_seq_table([1024, 2048, 9000, 512])
+    o = oplan.plan_step(t, 16384, 1, 1, 2, 2)
+    lay = olssp.layout(o, t["lens"], 2, 4096, 2)
+    dp = sorted(int(t["lens"][i]) for i in range(4) if lay["state"][i] == 0)
+    sp = sorted(int(t["lens"][i]) for i in range(4) if lay["state"][i] == 1)
+    assert dp == [512, 1024, 2048] and sp == [9000]
+    # the 9000-token sample is split 4500/4500 over the group of 2
+    i9 = int(np.flatnonzero(t["lens"] == 9000)[0])
+    assert lay["recv_rows"][:, 1].sum() == 0
+    assert sum(n for (i, _, n, *_r) in lay["fragments"] if i == i9) == 9000
+    pure = olssp.layout(o, t["lens"], 2, 9000, 2)
+    assert (pure["state"][pure["state"] >= 0] == 0).all()
+
+
+@pytest.mark.parametrize("sp_enc", [1, 2, 4])
+def test_lssp_layout_properties_on_golden_steps(sp_enc):
+    """Conservation (every encoded sample in exactly one state), every encoder row
+    written once and returned once, eta = inf equals the plain layout, and the
+    packed LLM input is independent of the encoder's DP/SP split."""
+    checked = 0
+    for name, st, t, _ in golden_steps():
+        world = st["world"]
+        if world % sp_enc or name not in ("cfg5", "cfg4", "cfg3") or st["step"] > 0:
+            continue
+        o = oracle_plan(t, st)
+        lens = np.asarray(t["lens"], np.int64)
+        items = np.flatnonzero(o["enc"] >= 0)
+        eta = int(np.median(lens[items])) if len(items) else 0
+        lay = olssp.layout(o, lens, world, eta, sp_enc)
+        assert set(lay["state"][items].tolist()) <= {0, 1}
+        # every encoder row of every rank covered exactly once by the fragments
+        for r in range(world):
+            for g in range(2):
+                cover = np.zeros(int(lay["recv_rows"][r, g]), np.int64)
+                for (i, t0, n, sr, srow, dr, drow, gg) in lay["fragments"]:
+                    if sr == r and gg == g:
+                        cover[srow:srow + n] += 1
+                assert (cover == 1).all()
+        plain = olssp.layout(o, lens, world, int(lens.max()) + 1, sp_enc)
+        assert [f[4] for f in plain["fragments"]] == [p[1] for p in o["pieces"]]
+        assert np.array_equal(plain["recv_rows"], o["recv_rows"])
+        # LLM input identical with and without the split (narrow rows)
+        rs = np.random.RandomState(3)
+        ar = [[rs.randint(0, 2 ** 16, size=(int(o["arena_rows"][r, g]), 4)).astype(np.uint16)
+               for g in range(2)] for r in range(world)]
+        _, _, llm_a = odp.run_world(o, t, world, ar, (4, 4), (8, 8), 8)
+        _, _, llm_b = olssp.run_world(o, lay, t, world, ar, (4, 4), (8, 8), 8)
+        assert all(np.array_equal(a, b) for a, b in zip(llm_a, llm_b))
+        # dispatch tables move every loader row exactly once
+        moved = sum(int(d[:, 2].sum()) for d in
+                    (olssp.dispatch_by_rank(o, lay, lens, r) for r in range(world)))
+        assert moved == int(lens[items].sum())
+        checked += 1
+    assert checked >= 2
