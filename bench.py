@@ -47,6 +47,10 @@ def parse():
                     help="encoder balancing: locality-first LPT (default), LPT or KK")
     ap.add_argument("--hang-dump", type=float, default=0.0,
                     help="dump Python stacks after this many seconds (debug)")
+    ap.add_argument("--lssp-eta", type=int, default=-1,
+                    help="LSSP eta split: samples longer than this are encoded as token "
+                         "shards over encoder groups (-1: off)")
+    ap.add_argument("--lssp-sp", type=int, default=0, help="LSSP group size (0: all ranks)")
     ap.add_argument("--graphs", type=int, default=0,
                     help="1: replay one captured CUDA graph per pipelined step")
     return ap.parse_args()
@@ -238,7 +242,9 @@ def run_ours(args):
 
     path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
                    d_in=d_in, d_enc=d_enc, d_llm=d_llm, projector=projector, device=dev,
-                   group=group, method=args.method)
+                   group=group, method=args.method,
+                   lssp_eta=args.lssp_eta if args.lssp_eta >= 0 else None,
+                   lssp_sp=args.lssp_sp or world)
     if projector:
         gen = torch.Generator(device=dev).manual_seed(77)
         for g in range(2):
@@ -354,7 +360,13 @@ def run_ours(args):
         dist.barrier()
 
     # per-stage breakdown (separate untimed pass, CUDA events between stages)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    # (+ the gradient return of SURVEY §8f-1: dY at the placeholders back to the
+    # encoder ranks — measured here, not part of the headline step)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    dy = torch.randn(path.max_llm_rows, d_llm, device=dev).to(torch.bfloat16)
+    if not path.staged:  # allocate the gradient windows (collective) and warm up
+        path.grad_return(path.plan(dtabs[0], stream), dy, stream)
+        torch.cuda.synchronize()
     for k in range(args.steps):
         i = (args.warmup + k) % n_distinct
         ev[k][0].record(stream)
@@ -364,10 +376,14 @@ def run_ours(args):
         ev[k][2].record(stream)
         path.return_scatter(p, stream)
         ev[k][3].record(stream)
+        if not path.staged:  # gradient path is defined for final-row layouts
+            path.grad_return(p, dy, stream)
+        ev[k][4].record(stream)
     torch.cuda.synchronize()
     stages = {nm: float(np.mean([e[j].elapsed_time(e[j + 1]) for e in ev]))
               for j, nm in enumerate(("plan_ms", "pack_dispatch_ms",
-                                      "projector_scatter_ms" if projector else "return_scatter_ms"))}
+                                      "projector_scatter_ms" if projector else "return_scatter_ms",
+                                      "grad_return_ms"))}
     # dominant kernel = the return kernel (return+scatter copy, or the projector
     # GEMM), CUDA events on its stream around the launch, over the timed steps
     dom_ms = [a.elapsed_time(b) for a, b in ev_dom] if not graphs else \
@@ -432,6 +448,8 @@ def run_ours(args):
                    "modality_tokens_per_step": M_total / args.steps,
                    "planner": "pipelined on a side stream" if args.pipeline else "in-line",
                    "balance": args.method,
+                   "lssp": ({"eta": args.lssp_eta, "group": args.lssp_sp or world}
+                            if args.lssp_eta >= 0 else None),
                    "launch": "one CUDA graph per step" if graphs is not None else "eager",
                    "llm_tokens_per_step": T_total / args.steps,
                    "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"},

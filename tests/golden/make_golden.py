@@ -144,7 +144,29 @@ def gen_misc():
     _dump("misc.json", dict(recipes=recipes, build_global_batch=gb))
 
 
+def gen_export():
+    """export_batch (workload.py:308-324) of two chained cfg5 steps at dp=8: the
+    reference's JSONL bytes, with the batch and the sample map that made them."""
+    import tempfile
+    reg, sched = configs.build(ref, "cfg5")
+    cfg = configs.CONFIGS["cfg5"]
+    carry, recs = None, []
+    for step in range(2):
+        drawn = []
+        batch, carry_next = ref.generate_batch(reg, sched, step, cfg["seed"], 16, 8, 1,
+                                               configs.CAPACITY, carry, drawn)
+        samples = {s.id: s for s in drawn}
+        with tempfile.NamedTemporaryFile("r", suffix=".jsonl") as fh:
+            ref.export_batch(batch, samples, fh.name)
+            text = open(fh.name).read()
+        recs.append(dict(step=step, dp=8, mbs=1, capacity=configs.CAPACITY,
+                         seqs=_seqs(batch.sequences), samples=_samples(drawn), jsonl=text))
+        carry = carry_next
+    _dump("export.json", dict(batches=recs))
+
+
 if __name__ == "__main__":
     gen_configs()
     gen_pack_cases()
     gen_misc()
+    gen_export()

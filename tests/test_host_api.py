@@ -83,6 +83,19 @@ def test_export_batch_schema(tmp_path):
                              {"modality": None, "sample": 2, "tokens": 4}]}
 
 
+def test_export_batch_matches_reference_bytes(tmp_path):
+    """export_batch JSONL byte-identical to the reference's (tests/golden/export.json,
+    written by the reference's own export_batch on two chained cfg5 steps)."""
+    from tests.helpers import golden
+    for rec in golden("export.json")["batches"]:
+        seqs = [W.PackedSequence(rec["capacity"], [tuple(sp) for sp in q]) for q in rec["seqs"]]
+        b = W.GlobalBatch(rec["step"], seqs, rec["dp"], rec["mbs"])
+        samples = {i: W.Sample(i, W.Modality(m), d, L) for i, m, d, L in rec["samples"]}
+        out = tmp_path / f"b{rec['step']}.jsonl"
+        W.export_batch(b, samples, out)
+        assert out.read_text() == rec["jsonl"]
+
+
 def test_capi_exports_every_declared_symbol():
     from paper_2605_08962_b200 import _lib
     hdr = open(os.path.join(ROOT, "include", "mux_b200.h")).read()
