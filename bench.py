@@ -51,6 +51,9 @@ def parse():
                     help="LSSP eta split: samples longer than this are encoded as token "
                          "shards over encoder groups (-1: off)")
     ap.add_argument("--lssp-sp", type=int, default=0, help="LSSP group size (0: all ranks)")
+    ap.add_argument("--reshard", default="ulysses", choices=["ulysses", "cp_hybrid"],
+                    help="LLM placement over each replica's sp ranks")
+    ap.add_argument("--cp-threshold", type=int, default=0, help="CpHybrid threshold (0: C/sp)")
     ap.add_argument("--graphs", type=int, default=0,
                     help="1: replay one captured CUDA graph per pipelined step")
     return ap.parse_args()
@@ -244,7 +247,8 @@ def run_ours(args):
                    d_in=d_in, d_enc=d_enc, d_llm=d_llm, projector=projector, device=dev,
                    group=group, method=args.method,
                    lssp_eta=args.lssp_eta if args.lssp_eta >= 0 else None,
-                   lssp_sp=args.lssp_sp or world)
+                   lssp_sp=args.lssp_sp or world, reshard=args.reshard,
+                   cp_threshold=args.cp_threshold)
     if projector:
         gen = torch.Generator(device=dev).manual_seed(77)
         for g in range(2):
@@ -450,6 +454,7 @@ def run_ours(args):
                    "balance": args.method,
                    "lssp": ({"eta": args.lssp_eta, "group": args.lssp_sp or world}
                             if args.lssp_eta >= 0 else None),
+                   "reshard": args.reshard if sp > 1 else None,
                    "launch": "one CUDA graph per step" if graphs is not None else "eager",
                    "llm_tokens_per_step": T_total / args.steps,
                    "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"},

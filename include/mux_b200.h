@@ -103,7 +103,15 @@ typedef struct {
    * (1..MUX_LSSP_MAX, divides world; 0 = off); samples longer than lssp_eta
    * are encoded in the SP state, one token shard per group member. */
   int32_t lssp_sp, lssp_eta;
+  /* LLM-side placement (reshard.plan_reshard): Ulysses
+   * uniform shards (default) or CpHybrid over the replica's sp ranks (long
+   * samples, len > cp_threshold, split sp ways; short ones whole by LPT on the
+   * residual loads).  cp_threshold 0 = capacity / sp. */
+  int32_t reshard, cp_threshold;
 } mux_plan_cfg;
+
+#define MUX_RESHARD_ULYSSES 0
+#define MUX_RESHARD_CP_HYBRID 1
 
 #define MUX_LSSP_MAX 8
 
@@ -142,6 +150,13 @@ typedef struct {
    * S*lssp_sp segments and the return/gradient tables S*(sp+1+lssp_sp). */
   int64_t lssp_state;                               /* int32[S]           */
   int64_t lssp_row;                                 /* int64[S*MUX_LSSP_MAX] */
+  /* CpHybrid LLM pieces per sample (reshard == MUX_RESHARD_CP_HYBRID): count,
+   * then per piece the CP rank index k, first token, tokens and LLM row on
+   * rank (replica * sp + k).  shard_len then holds each (sequence, k) load
+   * and row_base its first row. */
+  int64_t lp_n;                                     /* int32[S]           */
+  int64_t lp_k, lp_t0, lp_len;                      /* int32[S*sp]        */
+  int64_t lp_row;                                   /* int64[S*sp]        */
   int64_t total;
 } mux_plan_layout;
 

@@ -33,7 +33,7 @@ class PlanCfg(C.Structure):
         ("row_bytes_in", C.c_int32 * N_GROUPS), ("row_bytes_ret", C.c_int32 * N_GROUPS),
         ("chunk_bytes", C.c_int32), ("ret_mode", C.c_int32),
         ("row_bytes_grad", C.c_int32 * N_GROUPS), ("lssp_sp", C.c_int32),
-        ("lssp_eta", C.c_int32)]
+        ("lssp_eta", C.c_int32), ("reshard", C.c_int32), ("cp_threshold", C.c_int32)]
 
 
 LAYOUT_FIELDS = (
@@ -44,7 +44,8 @@ LAYOUT_FIELDS = (
     "dseg_rows", "dseg_group", "dseg_dst_rank", "dseg_chunk0", "rseg_src_row", "rseg_dst_row",
     "rseg_rows", "rseg_group", "rseg_dst_rank", "rseg_chunk0", "gseg_src_row", "gseg_dst_row",
     "gseg_rows", "gseg_group", "gseg_dst_rank", "gseg_chunk0", "lssp_state", "lssp_row",
-    "total")
+    "lp_n", "lp_k", "lp_t0", "lp_len", "lp_row", "total")
+RESHARD = {"ulysses": 0, "cp_hybrid": 1}
 LSSP_MAX = 8
 
 

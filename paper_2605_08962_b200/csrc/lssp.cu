@@ -43,21 +43,15 @@ __device__ __forceinline__ void shard_of(int L, int G, int k, int& s0, int& n) {
 
 // Every fragment of sample i (LLM piece x encoder shard), in token order:
 // f(t0, n, src_rank, src_row, dst_rank, dst_row).
+// The LLM pieces of sample i come from the Ulysses shard geometry or, with
+// CpHybrid, from the piece table reshard.cu wrote.
 template <typename F>
 __device__ void for_fragments(const mux_plan_cfg& cfg, const Plan& p, int i, int L, int state,
-                              int enc, F&& f) {
-  const int sp = cfg.sp, P = cfg.gbs / cfg.dp, G = cfg.lssp_sp;
+                              int enc, int G, F&& f) {
+  const int sp = cfg.sp, P = cfg.gbs / cfg.dp;
   const int q = p.seq[i], off = p.off[i];
   const int base = enc - enc % G;
-  for (int t = 0; t < L;) {
-    const int pos = off + t;
-    int kk = 0;
-    for (int j = 0; j < sp; ++j)
-      if (p.shard_start[q * sp + j] <= pos) kk = j;
-    const int end = p.shard_start[q * sp + kk] + p.shard_len[q * sp + kk];
-    const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
-    const int dst = (q / P) * sp + kk;
-    const int64_t drow = p.row_base[q * sp + kk] + pos - p.shard_start[q * sp + kk];
+  auto piece = [&](int t, int n, int dst, int64_t drow) {
     if (state == 0) {
       f(t, n, enc, p.lssp_row[(int64_t)i * MUX_LSSP_MAX] + t, dst, drow);
     } else {
@@ -70,19 +64,36 @@ __device__ void for_fragments(const mux_plan_cfg& cfg, const Plan& p, int i, int
             drow + (a - t));
       }
     }
+  };
+  if (cfg.reshard == MUX_RESHARD_CP_HYBRID) {
+    const int np = p.lp_n[i];
+    for (int m = 0; m < np; ++m) {
+      const int64_t x = (int64_t)i * sp + m;
+      piece(p.lp_t0[x], p.lp_len[x], (q / P) * sp + p.lp_k[x], p.lp_row[x]);
+    }
+    return;
+  }
+  for (int t = 0; t < L;) {
+    const int pos = off + t;
+    int kk = 0;
+    for (int j = 0; j < sp; ++j)
+      if (p.shard_start[q * sp + j] <= pos) kk = j;
+    const int end = p.shard_start[q * sp + kk] + p.shard_len[q * sp + kk];
+    const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
+    piece(t, n, (q / P) * sp + kk, p.row_base[q * sp + kk] + pos - p.shard_start[q * sp + kk]);
     t += n;
   }
 }
 
 __global__ void __launch_bounds__(kLsspThreads, 1)
-    lssp_kernel(mux_plan_cfg cfg, const int32_t* __restrict__ lens, Plan p) {
+    lssp_kernel(mux_plan_cfg cfg, const int32_t* __restrict__ lens, Plan p, int G, int eta) {
   extern __shared__ __align__(16) unsigned char smem[];
   Item* it = reinterpret_cast<Item*>(smem);
   __shared__ int64_t s_warp[33];
   __shared__ unsigned long long s_dp[MUX_LSSP_MAX * MUX_N_GROUPS * 1 + 64];
   __shared__ unsigned long long s_sp[MUX_LSSP_MAX * MUX_N_GROUPS * 1 + 64];
   if (p.hdr[MUX_H_STATUS] != MUX_OK) return;  // the plan failed: leave it as is
-  const int S = cfg.S, W = cfg.world, G = cfg.lssp_sp, me = cfg.me, eta = cfg.lssp_eta;
+  const int S = cfg.S, W = cfg.world, me = cfg.me;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int r = tid; r < W * MUX_N_GROUPS; r += nt) s_dp[r] = s_sp[r] = 0;
   // stage: key (state, home, group), length, encoder offset
@@ -170,7 +181,7 @@ __global__ void __launch_bounds__(kLsspThreads, 1)
     int nr = 0, ng = 0;
     int64_t rchk = 0, gchk = 0;
     if (ki >= 0)
-      for_fragments(cfg, p, i, L, state, e, [&](int, int n, int src, int64_t, int dst, int64_t) {
+      for_fragments(cfg, p, i, L, state, e, G, [&](int, int n, int src, int64_t, int dst, int64_t) {
         if (src == me) {
           ++nr;
           rchk += ((int64_t)n * cfg.row_bytes_ret[g] + CH - 1) / CH;
@@ -215,7 +226,7 @@ __global__ void __launch_bounds__(kLsspThreads, 1)
     gcarry += tot;
     gchunks += tchk;
     if (nr || ng)
-      for_fragments(cfg, p, i, L, state, e,
+      for_fragments(cfg, p, i, L, state, e, G,
                     [&](int, int n, int src, int64_t srow, int dst, int64_t drow) {
                       if (src == me) {
                         const int64_t nb = (int64_t)n * cfg.row_bytes_ret[g];
@@ -276,7 +287,10 @@ __global__ void __launch_bounds__(kLsspThreads, 1)
 
 }  // namespace
 
-int launch_lssp(const mux_plan_cfg& cfg, const int32_t* lens, const Plan& p, cudaStream_t stream) {
+// Segment tables for encoder groups of G ranks and threshold eta (G = 1 and
+// eta = INT_MAX: every sample DP, i.e. the plain encoder layout).
+int launch_emit(const mux_plan_cfg& cfg, const int32_t* lens, const Plan& p, int G, int eta,
+                cudaStream_t stream) {
   const int smem = (cfg.S > 0 ? cfg.S : 1) * (int)sizeof(Item);
   static bool attr = false;
   if (!attr) {
@@ -286,9 +300,13 @@ int launch_lssp(const mux_plan_cfg& cfg, const int32_t* lens, const Plan& p, cud
   }
   int threads = ((cfg.S + 31) / 32) * 32;
   threads = threads < 128 ? 128 : (threads > kLsspThreads ? kLsspThreads : threads);
-  lssp_kernel<<<1, threads, smem, stream>>>(cfg, lens, p);
+  lssp_kernel<<<1, threads, smem, stream>>>(cfg, lens, p, G, eta);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
+}
+
+int launch_lssp(const mux_plan_cfg& cfg, const int32_t* lens, const Plan& p, cudaStream_t stream) {
+  return launch_emit(cfg, lens, p, cfg.lssp_sp, cfg.lssp_eta, stream);
 }
 
 }  // namespace mux

@@ -123,11 +123,18 @@ struct Plan {
   int32_t *ggroup, *grank;
   int32_t* lssp_state;
   int64_t* lssp_row;  // [S][MUX_LSSP_MAX]
+  int32_t *lp_n, *lp_k, *lp_t0, *lp_len;  // CpHybrid pieces [S][sp]
+  int64_t* lp_row;
 };
 
 Plan make_plan(void* base, const mux_plan_layout& L);
 // LSSP re-targeting of a step plan (lssp.cu), launched after plan_kernel.
 int launch_lssp(const mux_plan_cfg& cfg, const int32_t* lens, const Plan& p, cudaStream_t stream);
+int launch_emit(const mux_plan_cfg& cfg, const int32_t* lens, const Plan& p, int G, int eta,
+                cudaStream_t stream);
+// CpHybrid LLM placement (reshard.cu), then the segment tables (lssp.cu).
+int launch_cp_hybrid(const mux_plan_cfg& cfg, const int32_t* lens, const int64_t* ids,
+                     const Plan& p, cudaStream_t stream);
 Plan make_plan_const(const void* base, const mux_plan_layout& L);
 
 // Upper bounds used by the layout.

@@ -68,8 +68,15 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
                 c.lssp_sp, MUX_LSSP_MAX, c.world);
       return MUX_ERR_VALUE;
     }
-  } else if (c.lssp_sp != 0) {
-    set_error("LSSP applies to step plans only");
+    if (c.reshard != MUX_RESHARD_ULYSSES &&
+        (c.reshard != MUX_RESHARD_CP_HYBRID || c.ret_mode != MUX_RET_FINAL ||
+         c.cp_threshold < 0 || c.sp > 8)) {
+      set_error("reshard %d: need Ulysses (0) or CpHybrid (1) with final-row return, "
+                "cp_threshold >= 0, sp <= 8", c.reshard);
+      return MUX_ERR_VALUE;
+    }
+  } else if (c.lssp_sp != 0 || c.reshard != MUX_RESHARD_ULYSSES) {
+    set_error("LSSP and CpHybrid apply to step plans only");
     return MUX_ERR_VALUE;
   }
   const int64_t S = c.S > 0 ? c.S : 1;
@@ -137,6 +144,12 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->gseg_chunk0 = take(8 * (R + 1));
   L->lssp_state = take(4 * S);
   L->lssp_row = take(8 * S * MUX_LSSP_MAX);
+  const int64_t SP = S * (c.sp > 0 ? c.sp : 1);
+  L->lp_n = take(4 * S);
+  L->lp_k = take(4 * SP);
+  L->lp_t0 = take(4 * SP);
+  L->lp_len = take(4 * SP);
+  L->lp_row = take(8 * SP);
   L->total = o;
   return MUX_OK;
 }
@@ -200,6 +213,11 @@ Plan make_plan(void* b, const mux_plan_layout& L) {
   p.gchunk0 = at<int64_t>(b, L.gseg_chunk0);
   p.lssp_state = at<int32_t>(b, L.lssp_state);
   p.lssp_row = at<int64_t>(b, L.lssp_row);
+  p.lp_n = at<int32_t>(b, L.lp_n);
+  p.lp_k = at<int32_t>(b, L.lp_k);
+  p.lp_t0 = at<int32_t>(b, L.lp_t0);
+  p.lp_len = at<int32_t>(b, L.lp_len);
+  p.lp_row = at<int64_t>(b, L.lp_row);
   return p;
 }
 
@@ -1355,6 +1373,8 @@ extern "C" int mux_plan_step(const mux_plan_cfg* cfg, const int32_t* lens, const
   plan_kernel<<<grid, threads, smem, static_cast<cudaStream_t>(stream)>>>(
       *cfg, lens, mods, ids, carry_seq, chunk_off, p);
   MUX_CUDA(cudaGetLastError());
+  if (cfg->mode == MUX_MODE_STEP && cfg->reshard == MUX_RESHARD_CP_HYBRID)
+    return launch_cp_hybrid(*cfg, lens, ids, p, static_cast<cudaStream_t>(stream));
   if (cfg->mode == MUX_MODE_STEP && cfg->lssp_sp > 0)
     return launch_lssp(*cfg, lens, p, static_cast<cudaStream_t>(stream));
   return MUX_OK;

@@ -87,7 +87,8 @@ class MuxPath:
                  d_in=(588, 512), d_enc=(1280, 1280), d_llm: int = 4096,
                  projector: bool = False, device=None, group=None, max_rows: int | None = None,
                  wait_timeout_ms: int = 20000, projector_return: str | None = None,
-                 lssp_eta: int | None = None, lssp_sp: int = 1):
+                 lssp_eta: int | None = None, lssp_sp: int = 1, reshard: str = "ulysses",
+                 cp_threshold: int = 0):
         self.capacity, self.gbs, self.dp, self.sp = capacity, gbs, dp, sp
         self.world, self.rank, self.method, self.pooled = world, rank, method, pooled
         self.d_in, self.d_enc, self.d_llm = tuple(d_in), tuple(d_enc), d_llm
@@ -105,10 +106,14 @@ class MuxPath:
         if lssp_eta is not None and (lssp_sp < 1 or world % lssp_sp):
             raise ValueError(f"lssp_sp {lssp_sp} must divide world {world}")
         self.lssp_eta, self.lssp_sp = lssp_eta, lssp_sp
+        # LLM-side placement over each replica's sp ranks (reshard.plan_reshard)
+        self.reshard, self.cp_threshold = reshard, cp_threshold
         self.staged = bool(projector and world > 1 and mode == "staged")
         self.ret_mode = _lib.RET_STAGED if self.staged else _lib.RET_FINAL
         rows = max_rows or gbs * capacity                       # all batch tokens
         llm_rows = (gbs // dp) * capacity // sp + gbs // dp + 1  # one rank's shards
+        if reshard == "cp_hybrid":  # LPT may stack short samples on one CP rank
+            llm_rows = (gbs // dp) * capacity
         self.max_rows, self.max_llm_rows = rows, llm_rows
         self.num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.gemm_ctas = 0  # 0: one CTA per SM; plan_ahead() leaves one SM to the planner
@@ -168,7 +173,8 @@ class MuxPath:
                         row_bytes_ret=tuple(2 * d for d in self.d_ret), ret_mode=self.ret_mode,
                         row_bytes_grad=(2 * self.d_llm,) * N_GROUPS,
                         lssp_sp=self.lssp_sp if self.lssp_eta is not None else 0,
-                        lssp_eta=self.lssp_eta or 0)
+                        lssp_eta=self.lssp_eta or 0, reshard=self.reshard,
+                        cp_threshold=self.cp_threshold)
 
     @property
     def llm(self) -> _Window:

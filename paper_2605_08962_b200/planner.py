@@ -118,10 +118,15 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
              me: int = 0, mode: int = _lib.MODE_STEP, row_bytes_in=(1176, 1024),
              row_bytes_ret=(8192, 8192), chunk_bytes: int = DEFAULT_CHUNK_BYTES,
              ret_mode: int = _lib.RET_FINAL, row_bytes_grad=None, lssp_sp: int = 0,
-             lssp_eta: int = 0) -> PlanCfg:
+             lssp_eta: int = 0, reshard: str = "ulysses", cp_threshold: int = 0) -> PlanCfg:
     """One step's planner configuration (include/mux_b200.h mux_plan_cfg).
     lssp_sp > 0 turns on the LSSP eta split (samples longer than lssp_eta are
-    encoded as token shards over groups of lssp_sp ranks; oracle/lssp.py)."""
+    encoded as token shards over groups of lssp_sp ranks; oracle/lssp.py).
+    reshard: LLM placement over each replica's sp ranks, "ulysses" (uniform
+    shards) or "cp_hybrid" (long samples split, short ones whole by LPT;
+    oracle/cphybrid.py), cp_threshold 0 = capacity / sp."""
+    if reshard not in _lib.RESHARD:
+        raise ValueError(f"unknown reshard variant {reshard!r}")
     if method not in METHODS:
         raise ValueError(f"unknown balance method {method!r}")
     c = PlanCfg()
@@ -137,6 +142,7 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
     for g in range(_lib.N_GROUPS):
         c.row_bytes_grad[g] = 0 if row_bytes_grad is None else row_bytes_grad[g]
     c.lssp_sp, c.lssp_eta = int(lssp_sp), int(lssp_eta)
+    c.reshard, c.cp_threshold = _lib.RESHARD[reshard], int(cp_threshold)
     return c
 
 

@@ -20,6 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import dataplane as odp  # noqa: E402
+from oracle import cphybrid as ocph  # noqa: E402
 from oracle import lssp as olssp  # noqa: E402
 from oracle import planner as oplan  # noqa: E402
 from oracle import workload as owork  # noqa: E402
@@ -37,6 +38,7 @@ def main():
     narrow = "narrow" in sys.argv
     proj = "proj" in sys.argv
     lssp = "lssp" in sys.argv  # LSSP eta split: long samples sharded over encoder groups
+    cp = "cp" in sys.argv  # CpHybrid LLM placement instead of Ulysses shards
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -58,7 +60,8 @@ def main():
                    d_in=d_in, d_enc=d_enc, d_llm=d_llm, device=dev, group=dist.group.WORLD,
                    projector=proj,
                    projector_return="staged" if "staged" in sys.argv else "fused",
-                   lssp_eta=2048 if lssp else None, lssp_sp=world if lssp else 1)
+                   lssp_eta=2048 if lssp else None, lssp_sp=world if lssp else 1,
+                   reshard="cp_hybrid" if cp else "ulysses", cp_threshold=2048 if cp else 0)
     if proj:
         gw = torch.Generator().manual_seed(9)
         Ws = [(torch.randn(d_llm, d_enc[g], generator=gw) / d_enc[g] ** 0.5).to(torch.bfloat16)
@@ -78,6 +81,8 @@ def main():
         for method in (("lpt_local",) if proj else ("lpt", "kk", "lpt_local")):
             path.method = method
             o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
+            if cp:
+                o = ocph.place(o, t, gbs, dp, sp, configs.CAPACITY, 2048)
             lay = None
             if lssp:  # group of all ranks on even steps, pairs on odd steps
                 path.lssp_sp = world if step % 2 == 0 else 2

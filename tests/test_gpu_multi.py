@@ -18,13 +18,13 @@ def _ngpus():
 
 
 @pytest.mark.parametrize("config", ["cfg5", "cfg3", "cfg4", "cfg2 proj", "cfg2 proj staged",
-                                    "cfg5 lssp"])
+                                    "cfg5 lssp", "cfg4 cp", "cfg4 cp lssp"])
 def test_push_exchange_bit_exact(config):
     n = _ngpus()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(n, 8)
-    if config == "cfg4" and world % 4:
+    if config.startswith("cfg4") and world % 4:
         world = 2  # dp=2 x sp=1 fallback when sp=4 does not divide
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29611",

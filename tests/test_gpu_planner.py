@@ -277,3 +277,73 @@ def test_lssp_rejects_bad_groups(cuda_device):
                                lssp_sp=sp_enc, lssp_eta=10)
         with pytest.raises(ValueError, match="LSSP"):
             planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
+
+
+def cp_device_plan(t, cap, gbs, dp, sp, world, me, method, thr, lssp_sp=0, eta=0):
+    table = to_table(t)
+    cfg = planner.make_cfg(table, cap, gbs, dp, sp, world, 1, method, False, me,
+                           row_bytes_in=(1176, 1024), row_bytes_ret=(8192, 8192),
+                           reshard="cp_hybrid", cp_threshold=thr or 0,
+                           lssp_sp=lssp_sp, lssp_eta=eta)
+    plan = planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
+    plan.check(table)
+    return plan.host()
+
+
+def assert_cp_equal(d, c, t, me):
+    gb = c["shard_len"].size
+    assert np.array_equal(d["shard_len"][:gb], c["shard_len"].reshape(-1))
+    assert np.array_equal(d["row_base"][:gb], c["row_base"].reshape(-1))
+    assert np.array_equal(d["llm_rows"], c["llm_rows"])
+    assert np.array_equal(d["recv_rows"], c["recv_rows"])
+    assert np.array_equal(d["dseg"], odp.dispatch_by_rank(c, t["lens"], me))
+    assert np.array_equal(d["rseg"], odp.pieces_by_rank(c, me))
+    assert np.array_equal(d["gseg"], odp.grad_by_rank(c, me))
+
+
+@pytest.mark.parametrize("thr", [None, 1024, 1])
+def test_cp_hybrid_plan_matches_oracle(cuda_device, thr):
+    from oracle import cphybrid as ocph
+    n = 0
+    for name, st, t, _ in golden_steps():
+        for world, dp in ((2, 1), (4, 1), (4, 2), (8, 2), (8, 1)):
+            sp = world // dp
+            gbs = st["gbs"] * dp // st["dp"] if st["gbs"] % st["dp"] == 0 else st["gbs"]
+            try:
+                o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, "lpt")
+            except ValueError:
+                continue
+            c = ocph.place(o, t, gbs, dp, sp, configs.CAPACITY, thr)
+            for me in range(world):
+                d = cp_device_plan(t, configs.CAPACITY, gbs, dp, sp, world, me, "lpt", thr)
+                assert_cp_equal(d, c, t, me)
+                n += 1
+    assert n > 20
+
+
+def test_cp_hybrid_with_lssp_matches_oracle(cuda_device):
+    from oracle import cphybrid as ocph
+    from oracle import lssp as olssp
+    rs = np.random.RandomState(23)
+    checked = 0
+    for it in range(60):
+        t, cap = random_table(rs)
+        world, dp = [(2, 1), (4, 1), (4, 2), (8, 2)][it % 4]
+        sp = world // dp
+        gbs = dp * int(rs.randint(1, 3))
+        try:
+            o = oplan.plan_step(t, cap, gbs, dp, sp, world, 1, "lpt")
+        except ValueError:
+            continue
+        thr = int(rs.randint(0, cap + 1))
+        c = ocph.place(o, t, gbs, dp, sp, cap, thr)
+        me = int(rs.randint(0, world))
+        d = cp_device_plan(t, cap, gbs, dp, sp, world, me, "lpt", thr)
+        assert_cp_equal(d, c, t, me)
+        g = int(rs.choice([x for x in (1, 2, 4) if world % x == 0]))
+        eta = int(rs.randint(0, cap + 1))
+        lay = olssp.layout(c, t["lens"], world, eta, g)
+        d = cp_device_plan(t, cap, gbs, dp, sp, world, me, "lpt", thr, g, eta)
+        assert_lssp_equal(d, c, lay, t, me)
+        checked += 1
+    assert checked > 25

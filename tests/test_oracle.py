@@ -286,3 +286,48 @@ def test_lssp_layout_properties_on_golden_steps(sp_enc):
         assert moved == int(lens[items].sum())
         checked += 1
     assert checked >= 2
+
+
+# ---------------------------------------------------------------- CpHybrid placement
+from oracle import cphybrid as ocph  # noqa: E402
+
+
+def test_cphybrid_spec_kat():
+    """lengths [9000, 1024, 512], cp=4, threshold 4096 -> 9000 sharded
+    4-way (2250 each), 1024 and 512 whole on the least-loaded ranks."""
+    t = _one_seq_table([9000, 1024, 512])
+    o = oplan.plan_step(t, 16384, 1, 1, 4, 4)
+    c = ocph.place(o, t, 1, 1, 4, 16384, 4096)
+    i9 = 0
+    assert [(d, n) for (i, _, d, _, n) in c["pieces"] if i == i9] == [(k, 2250) for k in range(4)]
+    assert sorted(c["shard_len"][0].tolist()) == [2250, 2250, 2250 + 512, 2250 + 1024]
+    assert int(c["llm_rows"].sum()) == 10536
+
+
+def test_cphybrid_matches_plan_reshard_on_golden_steps():
+    """Same shard map as oracle plan_reshard's cp_hybrid (pinned vs the GPU planner),
+    and every LLM row of every rank written exactly once."""
+    n = 0
+    for name, st, t, _ in golden_steps():
+        if st["world"] != 1 or st["step"] > 1:
+            continue
+        for cp in (2, 4, 8):
+            for thr in (None, 1024):
+                o = oplan.plan_step(t, configs.CAPACITY, st["gbs"], 1, cp, cp)
+                c = ocph.place(o, t, st["gbs"], 1, cp, configs.CAPACITY, thr)
+                smap, loads = oplan.plan_reshard([[tuple(x) for x in q] for q in st["batch"]],
+                                                 cp, "cp_hybrid", thr, configs.CAPACITY)
+                assert c["shard_len"].tolist() == loads
+                ids = np.asarray(t["lens"]) * 0 + np.asarray(t["ids"])
+                for (i, src, d, drow, rows) in c["pieces"]:
+                    t0 = src - int(o["enc_off"][i])
+                    assert (d, t0, t0 + rows) in smap[int(ids[i])]
+                cover = [np.zeros(int(r), np.int64) for r in c["llm_rows"]]
+                for (i, src, d, drow, rows) in c["pieces"]:
+                    cover[d][drow:drow + rows] += 1
+                text = sum(int(L) for i, L in enumerate(t["lens"])
+                           if 0 <= o["seq"][i] < st["gbs"] and o["group"][i] < 0)
+                assert all((x <= 1).all() for x in cover)
+                assert sum(int(x.sum()) for x in cover) + text == int(c["llm_rows"].sum())
+                n += 1
+    assert n >= 12
