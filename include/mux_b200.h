@@ -76,7 +76,9 @@ extern "C" {
 #define MUX_H_GRAD_CHUNKS 17
 #define MUX_H_GRAD_BYTES 18
 #define MUX_H_GRAD_REMOTE 19
-#define MUX_H_STAMP0 20      /* 20..30: planner phase timestamps (globaltimer)  */
+#define MUX_H_STAMP0 20      /* 20..29: planner phase timestamps (globaltimer)  */
+#define MUX_H_N_TEXT 30      /* text segments of rank `me` (cfg.text_embed)      */
+#define MUX_H_TEXT_ROWS 31   /* text rows of rank `me`                          */
 #define MUX_H_SLOTS 32
 
 #define MUX_RET_FINAL 0  /* return rows go to their final packed-LLM rows           */
@@ -108,6 +110,10 @@ typedef struct {
    * samples, len > cp_threshold, split sp ways; short ones whole by LPT on the
    * residual loads).  cp_threshold 0 = capacity / sp. */
   int32_t reshard, cp_threshold;
+  /* 1: also emit rank `me`'s text segments (token offset -> LLM row) so
+   * mux_text_embed can gather the text tokens' embedding rows into the same
+   * packed LLM buffer. */
+  int32_t text_embed;
 } mux_plan_cfg;
 
 #define MUX_RESHARD_ULYSSES 0
@@ -157,6 +163,12 @@ typedef struct {
   int64_t lp_n;                                     /* int32[S]           */
   int64_t lp_k, lp_t0, lp_len;                      /* int32[S*sp]        */
   int64_t lp_row;                                   /* int64[S*sp]        */
+  /* text rows (cfg.text_embed): token-array offset of every text sample
+   * (table order over all text samples), then rank `me`'s text segments and
+   * their row prefix (tseg_row0[n] = total rows). */
+  int64_t text_off;                                 /* int64[S]           */
+  int64_t tseg_src, tseg_dst, tseg_rows;            /* int64[S*(sp+1)]    */
+  int64_t tseg_row0;                                /* int64[S*(sp+1)+1]  */
   int64_t total;
 } mux_plan_layout;
 
@@ -262,6 +274,17 @@ int mux_return_rows_ex(const mux_plan_cfg* cfg, const void* plan, int32_t group,
  * step table's int32 lengths (device). */
 int mux_stage_rows(const mux_plan_cfg* cfg, const void* plan, const int32_t* lens,
                    int32_t group, int64_t* row_dst, int64_t n_rows, void* stream);
+
+/* Text rows of the packed LLM input: for every text segment of rank `me`
+ * (plan made with cfg.text_embed = 1), out[dst_row + t, :] =
+ * table[tokens[src + t], :], t < rows.  tokens: int32 token ids of the
+ * step's text samples in table order (text_off); table: bf16 [vocab, d]
+ * embedding rows, replicated on every LLM rank; out: this rank's packed LLM
+ * buffer (row stride d).  Ids outside [0, vocab) are skipped and counted in
+ * *err (device int32).  d % 8 == 0. */
+int mux_text_embed(const mux_plan_cfg* cfg, const void* plan, const int32_t* tokens,
+                   const uint16_t* table, int64_t vocab, int32_t d, uint16_t* out, int32_t* err,
+                   void* stream);
 
 /* Projector fused with the scatter: for m < M,
  *   out_rank[row_dst[m] >> 40][row_dst[m] & (2^40-1), :] =

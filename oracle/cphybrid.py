@@ -86,7 +86,14 @@ def place(plan: dict, table: dict, gbs: int, dp: int, cp: int, capacity: int,
             if n > 0:
                 pieces.append((i, int(plan["enc_off"][i]) + t0, (q // P) * cp + k,
                                int(row_base[q, k]) + lrow, n))
+    text_pieces = []
+    for i in range(len(lens)):
+        if 0 <= seq[i] < gbs and plan["group"][i] < 0:
+            q = int(seq[i])
+            for (k, t0, n, lrow) in local[i]:
+                if n > 0:
+                    text_pieces.append((i, t0, (q // P) * cp + k, int(row_base[q, k]) + lrow, n))
     out = dict(plan)
-    out.update(pieces=pieces, llm_rows=llm_rows, row_base=row_base, shard_len=load,
-               cp_threshold=thr)
+    out.update(pieces=pieces, text_pieces=text_pieces, llm_rows=llm_rows, row_base=row_base,
+               shard_len=load, cp_threshold=thr)
     return out

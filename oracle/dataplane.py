@@ -138,3 +138,32 @@ def run_grad(plan: dict, world: int, dy, d_row):
         g, e = int(plan["group"][i]), int(plan["enc"][i])
         grad[e][g][src:src + n] = dy[dst_rank][dst_row:dst_row + n]
     return grad
+
+
+# ------------------------------------------------------------------ text rows
+def text_offsets(table: dict) -> np.ndarray:
+    """Offset of every text sample's token ids in the step's token array: the
+    text samples of the step table (batch or not) in table order."""
+    lens = np.asarray(table["lens"], np.int64)
+    text = np.array([m == 0 for m in table["mods"]], bool)
+    off = np.zeros(len(lens), np.int64)
+    off[1:] = np.cumsum(np.where(text, lens, 0))[:-1]
+    return np.where(text, off, -1)
+
+
+def text_by_rank(plan: dict, table: dict, me: int):
+    """Text segments of LLM rank `me`: (token offset, dst row, rows), table
+    order then token order."""
+    toff = text_offsets(table)
+    out = [(int(toff[i]) + t0, drow, n) for (i, t0, dr, drow, n) in plan["text_pieces"]
+           if dr == me]
+    return np.array(out, np.int64).reshape(-1, 3)
+
+
+def run_text(plan: dict, table: dict, world: int, tokens, emb, llm):
+    """Write every rank's text rows: llm[r][row] = emb[tokens[offset + t]]."""
+    toff = text_offsets(table)
+    for (i, t0, dr, drow, n) in plan["text_pieces"]:
+        ids = tokens[int(toff[i]) + t0:int(toff[i]) + t0 + n]
+        llm[dr][drow:drow + n] = emb[ids]
+    return llm

@@ -275,11 +275,25 @@ def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=F
             pieces.append((i, int(enc_off[i]) + t, rank,
                            int(row_base[q, k]) + pos - int(shard_start[q, k]), n))
             t += n
+    # text samples' LLM pieces (token offset in the sample, dst rank, dst row, rows):
+    # their rows come from the embedding table, not from an encoder
+    text_pieces = []
+    for i in range(S):
+        if not in_batch[i] or group[i] >= 0:
+            continue
+        q, r0, L = int(seq[i]), int(off[i]), int(lens[i])
+        t = 0
+        while t < L:
+            pos = r0 + t
+            rank, k = owner(q, pos)
+            n = min(L - t, int(shard_start[q, k] + shard_len[q, k]) - pos)
+            text_pieces.append((i, t, rank, int(row_base[q, k]) + pos - int(shard_start[q, k]), n))
+            t += n
     return dict(seq=seq, off=off, span=span, n_seq=n_seq, fills=fills, cu=cu,
                 in_batch=in_batch, origin=origin, origin_pos=origin_pos, group=group,
                 arena_off=arena_off, arena_rows=arena_rows, enc=enc, enc_off=enc_off,
                 recv_rows=recv_rows, llm_rows=llm_rows, shard_len=shard_len,
-                row_base=row_base, pieces=pieces, P=P)
+                row_base=row_base, pieces=pieces, text_pieces=text_pieces, P=P)
 
 
 def restore_order(plan):

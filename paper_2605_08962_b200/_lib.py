@@ -22,6 +22,7 @@ H_DISPATCH_CHUNKS, H_RETURN_CHUNKS, H_DISPATCH_BYTES, H_RETURN_BYTES = 5, 6, 7, 
 H_N_BATCH, H_DISPATCH_REMOTE, H_RETURN_REMOTE, H_RECV_ROWS0, H_RECV_ROWS1 = 9, 10, 11, 12, 13
 H_STAGE_ROWS0, H_STAGE_ROWS1 = 14, 15
 H_N_GRAD, H_GRAD_CHUNKS, H_GRAD_BYTES, H_GRAD_REMOTE, H_STAMP0 = 16, 17, 18, 19, 20
+H_N_TEXT, H_TEXT_ROWS = 30, 31
 RET_FINAL, RET_STAGED = 0, 1
 H_SLOTS = 32
 
@@ -33,7 +34,8 @@ class PlanCfg(C.Structure):
         ("row_bytes_in", C.c_int32 * N_GROUPS), ("row_bytes_ret", C.c_int32 * N_GROUPS),
         ("chunk_bytes", C.c_int32), ("ret_mode", C.c_int32),
         ("row_bytes_grad", C.c_int32 * N_GROUPS), ("lssp_sp", C.c_int32),
-        ("lssp_eta", C.c_int32), ("reshard", C.c_int32), ("cp_threshold", C.c_int32)]
+        ("lssp_eta", C.c_int32), ("reshard", C.c_int32), ("cp_threshold", C.c_int32),
+        ("text_embed", C.c_int32)]
 
 
 LAYOUT_FIELDS = (
@@ -44,7 +46,8 @@ LAYOUT_FIELDS = (
     "dseg_rows", "dseg_group", "dseg_dst_rank", "dseg_chunk0", "rseg_src_row", "rseg_dst_row",
     "rseg_rows", "rseg_group", "rseg_dst_rank", "rseg_chunk0", "gseg_src_row", "gseg_dst_row",
     "gseg_rows", "gseg_group", "gseg_dst_rank", "gseg_chunk0", "lssp_state", "lssp_row",
-    "lp_n", "lp_k", "lp_t0", "lp_len", "lp_row", "total")
+    "lp_n", "lp_k", "lp_t0", "lp_len", "lp_row", "text_off", "tseg_src", "tseg_dst",
+    "tseg_rows", "tseg_row0", "total")
 RESHARD = {"ulysses": 0, "cp_hybrid": 1}
 LSSP_MAX = 8
 
@@ -85,6 +88,8 @@ _SIGS = [
                                       _P]),
     ("mux_return_rows", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, C.c_int64, _P]),
     ("mux_stage_rows", C.c_int, [C.POINTER(PlanCfg), _P, _P, C.c_int32, _P, C.c_int64, _P]),
+    ("mux_text_embed", C.c_int, [C.POINTER(PlanCfg), _P, _P, _P, C.c_int64, C.c_int32, _P, _P,
+                                 _P]),
     ("mux_proj_scatter", C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P,
                                    C.c_int32, _P]),
     ("mux_proj_scatter_dev", C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P,

@@ -41,17 +41,40 @@ __device__ __forceinline__ void shard_of(int L, int G, int k, int& s0, int& n) {
   n = b + (k < r ? 1 : 0);
 }
 
+// The LLM pieces of batch sample i in token order, f(t0, n, dst_rank, dst_row):
+// from the Ulysses shard geometry or, with CpHybrid, the piece table
+// reshard.cu wrote.
+template <typename F>
+__device__ void for_llm_pieces(const mux_plan_cfg& cfg, const Plan& p, int i, int L, F&& f) {
+  const int sp = cfg.sp, P = cfg.gbs / cfg.dp;
+  const int q = p.seq[i], off = p.off[i];
+  if (cfg.reshard == MUX_RESHARD_CP_HYBRID) {
+    const int np = p.lp_n[i];
+    for (int m = 0; m < np; ++m) {
+      const int64_t x = (int64_t)i * sp + m;
+      f(p.lp_t0[x], p.lp_len[x], (q / P) * sp + p.lp_k[x], p.lp_row[x]);
+    }
+    return;
+  }
+  for (int t = 0; t < L;) {
+    const int pos = off + t;
+    int kk = 0;
+    for (int j = 0; j < sp; ++j)
+      if (p.shard_start[q * sp + j] <= pos) kk = j;
+    const int end = p.shard_start[q * sp + kk] + p.shard_len[q * sp + kk];
+    const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
+    f(t, n, (q / P) * sp + kk, p.row_base[q * sp + kk] + pos - p.shard_start[q * sp + kk]);
+    t += n;
+  }
+}
+
 // Every fragment of sample i (LLM piece x encoder shard), in token order:
 // f(t0, n, src_rank, src_row, dst_rank, dst_row).
-// The LLM pieces of sample i come from the Ulysses shard geometry or, with
-// CpHybrid, from the piece table reshard.cu wrote.
 template <typename F>
 __device__ void for_fragments(const mux_plan_cfg& cfg, const Plan& p, int i, int L, int state,
                               int enc, int G, F&& f) {
-  const int sp = cfg.sp, P = cfg.gbs / cfg.dp;
-  const int q = p.seq[i], off = p.off[i];
   const int base = enc - enc % G;
-  auto piece = [&](int t, int n, int dst, int64_t drow) {
+  for_llm_pieces(cfg, p, i, L, [&](int t, int n, int dst, int64_t drow) {
     if (state == 0) {
       f(t, n, enc, p.lssp_row[(int64_t)i * MUX_LSSP_MAX] + t, dst, drow);
     } else {
@@ -64,25 +87,7 @@ __device__ void for_fragments(const mux_plan_cfg& cfg, const Plan& p, int i, int
             drow + (a - t));
       }
     }
-  };
-  if (cfg.reshard == MUX_RESHARD_CP_HYBRID) {
-    const int np = p.lp_n[i];
-    for (int m = 0; m < np; ++m) {
-      const int64_t x = (int64_t)i * sp + m;
-      piece(p.lp_t0[x], p.lp_len[x], (q / P) * sp + p.lp_k[x], p.lp_row[x]);
-    }
-    return;
-  }
-  for (int t = 0; t < L;) {
-    const int pos = off + t;
-    int kk = 0;
-    for (int j = 0; j < sp; ++j)
-      if (p.shard_start[q * sp + j] <= pos) kk = j;
-    const int end = p.shard_start[q * sp + kk] + p.shard_len[q * sp + kk];
-    const int n = (L - t) < (end - pos) ? (L - t) : (end - pos);
-    piece(t, n, (q / P) * sp + kk, p.row_base[q * sp + kk] + pos - p.shard_start[q * sp + kk]);
-    t += n;
-  }
+  });
 }
 
 __global__ void __launch_bounds__(kLsspThreads, 1)
@@ -106,6 +111,18 @@ __global__ void __launch_bounds__(kLsspThreads, 1)
     it[i].len = L;
     it[i].eoff = item ? p.enc_off[i] : 0;
     p.lssp_state[i] = state;
+  }
+  // token-array offset of every text sample (table order, batch or not)
+  if (cfg.text_embed) {
+    int64_t carry = 0;
+    for (int b0 = 0; b0 < S; b0 += nt) {
+      const int i = b0 + tid;
+      const bool text = i < S && p.group[i] < 0;
+      int64_t tot;
+      const int64_t pre = block_excl_scan(text ? lens[i] : 0, &tot, s_warp);
+      if (i < S) p.text_off[i] = text ? carry + pre : -1;
+      carry += tot;
+    }
   }
   __syncthreads();
   // DP rows: compacted in encoder order on the home rank
@@ -152,6 +169,7 @@ __global__ void __launch_bounds__(kLsspThreads, 1)
   int grad_rb[MUX_N_GROUPS];
   for (int g = 0; g < MUX_N_GROUPS; ++g)
     grad_rb[g] = cfg.row_bytes_grad[g] > 0 ? cfg.row_bytes_grad[g] : cfg.row_bytes_ret[g];
+  int64_t tcarry = 0, trows_all = 0;
   int64_t dcarry = 0, rcarry = 0, gcarry = 0, dchunks = 0, rchunks = 0, gchunks = 0;
   int64_t dbytes = 0, rbytes = 0, gbytes = 0, dremote = 0, rremote = 0, gremote = 0;
   for (int b0 = 0; b0 < S; b0 += nt) {
@@ -192,6 +210,34 @@ __global__ void __launch_bounds__(kLsspThreads, 1)
         }
       });
     int64_t tot, tchk;
+    // text rows of `me` (embedding gather, no encoder)
+    if (cfg.text_embed) {
+      const bool text = i < S && L > 0 && p.group[i] < 0 && p.seq[i] >= 0 && p.seq[i] < cfg.gbs;
+      int ntx = 0;
+      int64_t nrows = 0;
+      if (text)
+        for_llm_pieces(cfg, p, i, L, [&](int, int n, int dst, int64_t) {
+          if (dst == me) {
+            ++ntx;
+            nrows += n;
+          }
+        });
+      int64_t ts = tcarry + block_excl_scan(ntx, &tot, s_warp);
+      tcarry += tot;
+      int64_t tr = trows_all + block_excl_scan(nrows, &tchk, s_warp);
+      trows_all += tchk;
+      if (ntx)
+        for_llm_pieces(cfg, p, i, L, [&](int t, int n, int dst, int64_t drow) {
+          if (dst == me) {
+            p.tsrc[ts] = p.text_off[i] + t;
+            p.tdst[ts] = drow;
+            p.trows[ts] = n;
+            p.trow0[ts] = tr;
+            tr += n;
+            ++ts;
+          }
+        });
+    }
     int64_t slot = dcarry + block_excl_scan(nd, &tot, s_warp);
     int64_t c0 = dchunks + block_excl_scan(dchk, &tchk, s_warp);
     dcarry += tot;
@@ -279,6 +325,9 @@ __global__ void __launch_bounds__(kLsspThreads, 1)
     p.hdr[MUX_H_DISPATCH_REMOTE] = t[3];
     p.hdr[MUX_H_RETURN_REMOTE] = t[4];
     p.hdr[MUX_H_GRAD_REMOTE] = t[5];
+    p.hdr[MUX_H_N_TEXT] = cfg.text_embed ? tcarry : 0;
+    p.hdr[MUX_H_TEXT_ROWS] = cfg.text_embed ? trows_all : 0;
+    if (cfg.text_embed) p.trow0[tcarry] = trows_all;
     p.hdr[MUX_H_RECV_ROWS0] = (int64_t)(s_dp[me * MUX_N_GROUPS] + s_sp[me * MUX_N_GROUPS]);
     p.hdr[MUX_H_RECV_ROWS1] =
         (int64_t)(s_dp[me * MUX_N_GROUPS + 1] + s_sp[me * MUX_N_GROUPS + 1]);

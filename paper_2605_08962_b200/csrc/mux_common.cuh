@@ -125,6 +125,7 @@ struct Plan {
   int64_t* lssp_row;  // [S][MUX_LSSP_MAX]
   int32_t *lp_n, *lp_k, *lp_t0, *lp_len;  // CpHybrid pieces [S][sp]
   int64_t* lp_row;
+  int64_t *text_off, *tsrc, *tdst, *trows, *trow0;  // text segments of `me`
 };
 
 Plan make_plan(void* base, const mux_plan_layout& L);

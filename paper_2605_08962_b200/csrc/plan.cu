@@ -75,8 +75,8 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
                 "cp_threshold >= 0, sp <= 8", c.reshard);
       return MUX_ERR_VALUE;
     }
-  } else if (c.lssp_sp != 0 || c.reshard != MUX_RESHARD_ULYSSES) {
-    set_error("LSSP and CpHybrid apply to step plans only");
+  } else if (c.lssp_sp != 0 || c.reshard != MUX_RESHARD_ULYSSES || c.text_embed) {
+    set_error("LSSP, CpHybrid and text rows apply to step plans only");
     return MUX_ERR_VALUE;
   }
   const int64_t S = c.S > 0 ? c.S : 1;
@@ -150,6 +150,12 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
   L->lp_t0 = take(4 * SP);
   L->lp_len = take(4 * SP);
   L->lp_row = take(8 * SP);
+  const int64_t RT = S * ((c.sp > 0 ? c.sp : 1) + 1);
+  L->text_off = take(8 * S);
+  L->tseg_src = take(8 * RT);
+  L->tseg_dst = take(8 * RT);
+  L->tseg_rows = take(8 * RT);
+  L->tseg_row0 = take(8 * (RT + 1));
   L->total = o;
   return MUX_OK;
 }
@@ -218,6 +224,11 @@ Plan make_plan(void* b, const mux_plan_layout& L) {
   p.lp_t0 = at<int32_t>(b, L.lp_t0);
   p.lp_len = at<int32_t>(b, L.lp_len);
   p.lp_row = at<int64_t>(b, L.lp_row);
+  p.text_off = at<int64_t>(b, L.text_off);
+  p.tsrc = at<int64_t>(b, L.tseg_src);
+  p.tdst = at<int64_t>(b, L.tseg_dst);
+  p.trows = at<int64_t>(b, L.tseg_rows);
+  p.trow0 = at<int64_t>(b, L.tseg_row0);
   return p;
 }
 
@@ -1377,6 +1388,8 @@ extern "C" int mux_plan_step(const mux_plan_cfg* cfg, const int32_t* lens, const
     return launch_cp_hybrid(*cfg, lens, ids, p, static_cast<cudaStream_t>(stream));
   if (cfg->mode == MUX_MODE_STEP && cfg->lssp_sp > 0)
     return launch_lssp(*cfg, lens, p, static_cast<cudaStream_t>(stream));
+  if (cfg->mode == MUX_MODE_STEP && cfg->text_embed)  // text segments from the emitter
+    return launch_emit(*cfg, lens, p, 1, INT_MAX, static_cast<cudaStream_t>(stream));
   return MUX_OK;
 }
 

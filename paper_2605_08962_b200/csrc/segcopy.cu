@@ -324,6 +324,35 @@ __global__ void return_rows_kernel(Plan p, int group, int64_t* row_dst, int64_t 
   }
 }
 
+// Text rows of the packed LLM input: one warp per row, the embedding row of
+// the token id gathered with 128-bit loads.
+__global__ void __launch_bounds__(256) text_embed_kernel(Plan p, const int32_t* tokens,
+                                                         const uint16_t* table, int64_t vocab,
+                                                         int d, uint16_t* out, int32_t* err) {
+  const int64_t nseg = p.hdr[MUX_H_N_TEXT], rows = p.hdr[MUX_H_TEXT_ROWS];
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nv = d / 8;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    int64_t lo = 0, hi = nseg - 1;  // last segment with trow0 <= r
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (p.trow0[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int64_t t = r - p.trow0[lo];
+    const int32_t tok = tokens[p.tsrc[lo] + t];
+    if (tok < 0 || tok >= vocab) {
+      if (lane == 0) atomicAdd(err, 1);
+      continue;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(table + (int64_t)tok * d);
+    uint4* dst = reinterpret_cast<uint4*>(out + (p.tdst[lo] + t) * d);
+#pragma unroll 4
+    for (int v = lane; v < nv; v += 32) dst[v] = __ldg(src + v);
+  }
+}
+
 // Staged projector return: row_dst of the owner's staging rows of `group`.
 __global__ void stage_rows_kernel(Plan p, const int32_t* lens, int S, int me, int group,
                                   int64_t* row_dst, int64_t n_rows) {
@@ -471,6 +500,28 @@ extern "C" int mux_return_rows_ex(const mux_plan_cfg* cfg, const void* plan, int
   Plan p = make_plan_const(plan, L);
   return_rows_kernel<<<256, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, group, row_dst, n_rows,
                                                                          cfg->me, stage_slot);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_text_embed(const mux_plan_cfg* cfg, const void* plan, const int32_t* tokens,
+                              const uint16_t* table, int64_t vocab, int32_t d, uint16_t* out,
+                              int32_t* err, void* stream) {
+  if (!cfg->text_embed || cfg->mode != MUX_MODE_STEP) {
+    set_error("mux_text_embed needs a step plan made with text_embed = 1");
+    return MUX_ERR_VALUE;
+  }
+  if (d <= 0 || d % 8 || vocab <= 0 ||
+      (((uintptr_t)table | (uintptr_t)out) & 15) != 0) {
+    set_error("mux_text_embed: need d %% 8 == 0, vocab > 0, 16-byte aligned table and out");
+    return MUX_ERR_VALUE;
+  }
+  mux_plan_layout L;
+  int st = mux_plan_layout_of(cfg, &L);
+  if (st) return st;
+  Plan p = make_plan_const(plan, L);
+  text_embed_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      p, tokens, table, vocab, d, out, err);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

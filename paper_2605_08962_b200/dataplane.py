@@ -88,7 +88,7 @@ class MuxPath:
                  projector: bool = False, device=None, group=None, max_rows: int | None = None,
                  wait_timeout_ms: int = 20000, projector_return: str | None = None,
                  lssp_eta: int | None = None, lssp_sp: int = 1, reshard: str = "ulysses",
-                 cp_threshold: int = 0):
+                 cp_threshold: int = 0, text_embed: bool = False):
         self.capacity, self.gbs, self.dp, self.sp = capacity, gbs, dp, sp
         self.world, self.rank, self.method, self.pooled = world, rank, method, pooled
         self.d_in, self.d_enc, self.d_llm = tuple(d_in), tuple(d_enc), d_llm
@@ -108,6 +108,8 @@ class MuxPath:
         self.lssp_eta, self.lssp_sp = lssp_eta, lssp_sp
         # LLM-side placement over each replica's sp ranks (reshard.plan_reshard)
         self.reshard, self.cp_threshold = reshard, cp_threshold
+        # text tokens' embedding rows gathered into the same packed LLM buffer
+        self.text_embed = text_embed
         self.staged = bool(projector and world > 1 and mode == "staged")
         self.ret_mode = _lib.RET_STAGED if self.staged else _lib.RET_FINAL
         rows = max_rows or gbs * capacity                       # all batch tokens
@@ -174,7 +176,7 @@ class MuxPath:
                         row_bytes_grad=(2 * self.d_llm,) * N_GROUPS,
                         lssp_sp=self.lssp_sp if self.lssp_eta is not None else 0,
                         lssp_eta=self.lssp_eta or 0, reshard=self.reshard,
-                        cp_threshold=self.cp_threshold)
+                        cp_threshold=self.cp_threshold, text_embed=self.text_embed)
 
     @property
     def llm(self) -> _Window:
@@ -400,6 +402,29 @@ class MuxPath:
         self._ev_p[b] = ev_p
         self.last_llm = b
         return ev_p
+
+    # ------------------------------------------------------------- text rows
+    def embed_text(self, plan: Plan, tokens: torch.Tensor, table: torch.Tensor, stream=None):
+        """Text rows of this rank's packed LLM input: row <- table[token id] for
+        every text token this rank owns (needs text_embed=True).
+        tokens: int32 ids of the step's text samples in table order (device);
+        table: bf16 [vocab, d_llm] embedding rows (device, replicated)."""
+        if not self.text_embed:
+            raise ValueError("MuxPath(text_embed=True) is needed for embed_text")
+        assert tokens.dtype == torch.int32 and table.dtype == torch.bfloat16
+        assert table.shape[1] == self.d_llm and table.is_contiguous()
+        if getattr(self, "text_err", None) is None:
+            self.text_err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _lib.check(_lib.lib().mux_text_embed(
+            C.byref(plan.cfg), plan.ptr, tokens.data_ptr(), table.data_ptr(), table.shape[0],
+            self.d_llm, self.llm.tensor.data_ptr(), self.text_err.data_ptr(),
+            _stream_ptr(stream)), "mux_text_embed")
+
+    def check_text(self):
+        """Raise if any token id was outside the embedding table (synchronises)."""
+        if getattr(self, "text_err", None) is not None and int(self.text_err.item()):
+            raise ValueError(f"{int(self.text_err.item())} text rows had token ids outside "
+                             "the embedding table")
 
     # --------------------------------------------------------- gradient return
     def _ensure_grad(self):

@@ -118,7 +118,8 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
              me: int = 0, mode: int = _lib.MODE_STEP, row_bytes_in=(1176, 1024),
              row_bytes_ret=(8192, 8192), chunk_bytes: int = DEFAULT_CHUNK_BYTES,
              ret_mode: int = _lib.RET_FINAL, row_bytes_grad=None, lssp_sp: int = 0,
-             lssp_eta: int = 0, reshard: str = "ulysses", cp_threshold: int = 0) -> PlanCfg:
+             lssp_eta: int = 0, reshard: str = "ulysses", cp_threshold: int = 0,
+             text_embed: bool = False) -> PlanCfg:
     """One step's planner configuration (include/mux_b200.h mux_plan_cfg).
     lssp_sp > 0 turns on the LSSP eta split (samples longer than lssp_eta are
     encoded as token shards over groups of lssp_sp ranks; oracle/lssp.py).
@@ -143,6 +144,7 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
         c.row_bytes_grad[g] = 0 if row_bytes_grad is None else row_bytes_grad[g]
     c.lssp_sp, c.lssp_eta = int(lssp_sp), int(lssp_eta)
     c.reshard, c.cp_threshold = _lib.RESHARD[reshard], int(cp_threshold)
+    c.text_embed = int(bool(text_embed))
     return c
 
 
@@ -160,7 +162,8 @@ class Plan:
            "dseg_dst_rank", "rseg_group", "rseg_dst_rank", "chunk_nbins", "gseg_group",
            "gseg_dst_rank", "lssp_state")
     I64 = ("arena_off", "enc_off", "llm_row", "row_base", "arena_rows", "recv_rows", "llm_rows",
-           "lssp_row", "dseg_src_row", "dseg_dst_row", "dseg_rows", "rseg_src_row", "rseg_dst_row",
+           "lssp_row", "text_off", "tseg_src", "tseg_dst", "tseg_rows", "tseg_row0",
+           "dseg_src_row", "dseg_dst_row", "dseg_rows", "rseg_src_row", "rseg_dst_row",
            "rseg_rows", "dseg_chunk0", "rseg_chunk0", "gseg_src_row", "gseg_dst_row",
            "gseg_rows", "gseg_chunk0")
 
@@ -225,6 +228,12 @@ class Plan:
                                     self.view("dseg_group", nd).cpu().numpy().astype(np.int64),
                                     self.view("dseg_dst_rank", nd).cpu().numpy().astype(np.int64)],
                                    axis=1) if nd else np.zeros((0, 5), np.int64)
+            if c.text_embed:
+                nt = int(h[_lib.H_N_TEXT])
+                out["text_off"] = self.view("text_off", S).cpu().numpy()
+                out["tseg"] = np.stack([self.view(k, nt).cpu().numpy() for k in (
+                    "tseg_src", "tseg_dst", "tseg_rows")], axis=1) if nt else \
+                    np.zeros((0, 3), np.int64)
             if c.lssp_sp > 0:
                 out["lssp_state"] = self.view("lssp_state", S).cpu().numpy()
                 out["lssp_row"] = self.view("lssp_row", S * _lib.LSSP_MAX).cpu().numpy() \

@@ -145,3 +145,54 @@ def test_dataplane_lssp_one_gpu(cuda_device, eta):
             assert np.array_equal(got, want[0][g]), f"gradient group {g}"
         return
     raise AssertionError("target1 golden step missing")
+
+
+def test_dataplane_with_text_rows(cuda_device):
+    """The whole packed LLM input of a step: modality rows from the return path,
+    text rows gathered from a bf16 embedding table by token id."""
+    for name, st, t, _ in golden_steps():
+        if name != "cfg2" or st["world"] != 1 or st["step"] != 0:
+            continue
+        cap, gbs, d_in, d_llm = configs.CAPACITY, st["gbs"], (20, 8), 64
+        o = oplan.plan_step(t, cap, gbs, 1, 1, 1, 1, "lpt")
+        assert o["text_pieces"]
+        arenas_cpu = [payload(int(o["arena_rows"][0, g]), d_in[g], 100 + g) for g in range(2)]
+        path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_llm=d_llm, method="lpt",
+                       text_embed=True)
+        table = to_table(t)
+        dtab = planner.DeviceTable(table, "cuda")
+        plan = path.plan(dtab)
+        plan.check(table)
+        vocab = 5000
+        emb = payload(vocab, d_llm, 11)
+        n_text = int(sum(int(L) for L, m in zip(t["lens"], t["mods"]) if m == 0))
+        tokens = torch.randint(0, vocab, (max(n_text, 1),), generator=torch.Generator()
+                               .manual_seed(4), dtype=torch.int32)
+        path.llm_view().zero_()
+        path.dispatch(plan, [a.cuda() for a in arenas_cpu])
+        path.encode_standin(plan, dtab)
+        path.return_scatter(plan)
+        path.embed_text(plan, tokens.cuda(), emb.cuda())
+        torch.cuda.synchronize()
+        path.check_text()
+        ar = [[a.view(torch.int16).numpy().view(np.uint16) for a in arenas_cpu]]
+        _, _, llm = odp.run_world(o, t, 1, ar, d_in, (d_llm, d_llm), d_llm)
+        llm = odp.run_text(o, t, 1, tokens.numpy(), emb.view(torch.int16).numpy().view(np.uint16),
+                           llm)
+        n = int(o["llm_rows"][0])
+        got = path.llm_view(n).cpu().view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got, llm[0])
+        # every LLM row is written: modality + text rows fill the packed buffer
+        assert int(plan.header()[_lib_H_TEXT_ROWS()]) + int(o["recv_rows"].sum()) == n
+        bad = tokens.clone()
+        bad[0] = vocab
+        path.embed_text(plan, bad.cuda(), emb.cuda())
+        with pytest.raises(ValueError, match="outside"):
+            path.check_text()
+        return
+    raise AssertionError("cfg2 golden step missing")
+
+
+def _lib_H_TEXT_ROWS():
+    from paper_2605_08962_b200 import _lib
+    return _lib.H_TEXT_ROWS

@@ -347,3 +347,33 @@ def test_cp_hybrid_with_lssp_matches_oracle(cuda_device):
         assert_lssp_equal(d, c, lay, t, me)
         checked += 1
     assert checked > 25
+
+
+@pytest.mark.parametrize("reshard", ["ulysses", "cp_hybrid"])
+def test_text_segments_match_oracle(cuda_device, reshard):
+    from oracle import cphybrid as ocph
+    n = 0
+    for name, st, t, _ in golden_steps():
+        for world, dp in ((1, 1), (2, 2), (4, 2), (4, 1)):
+            sp = world // dp
+            gbs = st["gbs"] * dp // st["dp"] if st["gbs"] % st["dp"] == 0 else st["gbs"]
+            try:
+                o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, "lpt")
+            except ValueError:
+                continue
+            if reshard == "cp_hybrid":
+                o = ocph.place(o, t, gbs, dp, sp, configs.CAPACITY)
+            table = to_table(t)
+            for me in range(world):
+                cfg = planner.make_cfg(table, configs.CAPACITY, gbs, dp, sp, world, 1, "lpt",
+                                       False, me, reshard=reshard, text_embed=True)
+                plan = planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
+                plan.check(table)
+                d = plan.host()
+                toff = odp.text_offsets(t)
+                text = toff >= 0
+                assert np.array_equal(d["text_off"][text], toff[text])
+                assert np.array_equal(d["tseg"], odp.text_by_rank(o, t, me))
+                assert np.array_equal(d["rseg"], odp.pieces_by_rank(o, me))
+                n += 1
+    assert n > 20
