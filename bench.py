@@ -63,6 +63,18 @@ def parse():
 # workload
 # ----------------------------------------------------------------------------
 
+def exchange_summary(plans_info, steps_idx, rank):
+    """Rank-local bytes per step of the two exchanges and the share leaving the
+    GPU over NVLink (the rest is a local HBM copy)."""
+    n = len(steps_idx)
+    avg = {k: sum(plans_info[i][k] for i in steps_idx) / n
+           for k in ("disp_bytes", "disp_remote", "ret_bytes", "ret_remote")}
+    return {"rank": rank, "dispatch_bytes": avg["disp_bytes"],
+            "dispatch_remote_frac": avg["disp_remote"] / max(avg["disp_bytes"], 1),
+            "return_bytes": avg["ret_bytes"],
+            "return_remote_frac": avg["ret_remote"] / max(avg["ret_bytes"], 1)}
+
+
 def measured_traffic(name, algo_bytes):
     """DRAM bytes per launch of the dominant kernel: the ncu-captured launch's
     traffic/algorithmic ratio (profiles/traffic.json) applied to this run's
@@ -459,6 +471,7 @@ def run_ours(args):
                    "llm_tokens_per_step": T_total / args.steps,
                    "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"},
         "roofline": roof,
+        "exchange": exchange_summary(plans_info, steps_idx, rank),
         "stages": stages,
         "gpu_launches": launches * args.steps,
         "host_enqueue_ms_per_step": host_ms / args.steps,

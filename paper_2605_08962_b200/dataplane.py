@@ -130,6 +130,9 @@ class MuxPath:
         # copy counters x3 tables, then the projector's completion ticket
         self.sync = torch.zeros(8, dtype=torch.int32, device=dev)
         self.kernel_events = None  # (start, end) CUDA events around the return kernel
+        # copy work unit and grid of the segment copies (tuning knobs; 0 = default grid)
+        self.chunk_bytes = int(os.environ.get("MUX_CHUNK_BYTES", "32768"))
+        self.copy_grid = int(os.environ.get("MUX_COPY_GRID", "0"))
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
@@ -176,7 +179,8 @@ class MuxPath:
                         row_bytes_grad=(2 * self.d_llm,) * N_GROUPS,
                         lssp_sp=self.lssp_sp if self.lssp_eta is not None else 0,
                         lssp_eta=self.lssp_eta or 0, reshard=self.reshard,
-                        cp_threshold=self.cp_threshold, text_embed=self.text_embed)
+                        cp_threshold=self.cp_threshold, text_embed=self.text_embed,
+                        chunk_bytes=self.chunk_bytes)
 
     @property
     def llm(self) -> _Window:
@@ -274,14 +278,14 @@ class MuxPath:
             ke[0].record(stream if stream is not None else torch.cuda.current_stream(self.device))
         if self.world == 1:
             _lib.check(L.mux_segcopy(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
-                                     dst.data_ptr(), 0, self.sync[2 * which:].data_ptr(), s),
-                       "mux_segcopy")
+                                     dst.data_ptr(), self.copy_grid,
+                                     self.sync[2 * which:].data_ptr(), s), "mux_segcopy")
             if ke is not None:
                 ke[1].record(stream if stream is not None else
                              torch.cuda.current_stream(self.device))
             return
         # beside an overlapped projector (which holds shared memory) copy CTAs stay lean
-        grid = -2 * self.num_sms if self.staged else 0
+        grid = -2 * self.num_sms if self.staged else self.copy_grid
         _lib.check(L.mux_segcopy_ex(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
                                     dst.data_ptr(), grid, -1, self.flag_ptrs.data_ptr(),
                                     self.sync[2 * which:].data_ptr(), self.epoch_ctr.data_ptr(),
