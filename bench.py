@@ -41,8 +41,9 @@ def parse():
     ap.add_argument("--distinct", type=int, default=8, help="distinct step inputs cycled")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--stages", action="store_true", help="per-stage timing breakdown")
-    ap.add_argument("--pipeline", type=int, default=1,
-                    help="1: plan step k+1 on a side stream during step k (default)")
+    ap.add_argument("--pipeline", type=int, default=2,
+                    help="1: plan step k+1 on a side stream during step k; 2 (default): also "
+                         "dispatch step k+1 under step k's return")
     ap.add_argument("--method", default="lpt_local", choices=["lpt", "kk", "lpt_local"],
                     help="encoder balancing: locality-first LPT (default), LPT or KK")
     ap.add_argument("--hang-dump", type=float, default=0.0,
@@ -260,7 +261,9 @@ def run_ours(args):
                    group=group, method=args.method,
                    lssp_eta=args.lssp_eta if args.lssp_eta >= 0 else None,
                    lssp_sp=args.lssp_sp or world, reshard=args.reshard,
-                   cp_threshold=args.cp_threshold)
+                   cp_threshold=args.cp_threshold, overlap_dispatch=args.pipeline >= 2)
+    if args.pipeline >= 2 and "MUX_DISPATCH_GRID" not in os.environ:
+        path.dispatch_grid = -2 * path.num_sms  # lean copy CTAs beside the GEMM
     if projector:
         gen = torch.Generator(device=dev).manual_seed(77)
         for g in range(2):
@@ -319,19 +322,9 @@ def run_ours(args):
             for k in range(n):
                 one_step(k0 + k, timed_dom[k] if timed_dom else None)
             return
-        R = path.RING
-        path.plan_ahead(dtabs[k0 % n_distinct], k0 % R, after=start_ev)
-        for k in range(n):
-            kk = k0 + k
-            if k + 1 < n:
-                path.plan_ahead(dtabs[(kk + 1) % n_distinct], (kk + 1) % R)
-            stream.wait_event(path._ready[kk % R])
-            p = path._ring[kk % R]
-            path.dispatch(p, arenas[kk % n_distinct], stream)
-            path.kernel_events = timed_dom[k] if timed_dom else None
-            ev = path.return_scatter(p, stream)
-            path.kernel_events = None
-            path._freed[kk % R] = ev
+        path.run_pipeline([(dtabs[(k0 + k) % n_distinct], arenas[(k0 + k) % n_distinct])
+                           for k in range(n)], kernel_events=timed_dom, start_event=start_ev,
+                          stream=stream)
 
     graphs = None
     if args.graphs and args.pipeline:
@@ -444,13 +437,16 @@ def run_ours(args):
         e2e = run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, world)
 
     # per step: fused planner (1) + dispatch copy (1, + flag wait at N>1) + return:
-    # projector: row map (side stream) + one grouped GEMM (+ signal + wait at N>1);
-    # otherwise one return copy (+ flag wait at N>1)
+    # projector: row map (side stream) + one grouped GEMM with the signal fused
+    # (+ flag wait at N>1); otherwise one return copy (+ flag wait at N>1);
+    # overlapped dispatch at N>1: + consumed signal + its wait
     launches = 1 + 1 + (1 if world > 1 else 0)
     if projector:
-        launches += 2 + (2 if world > 1 else 0)
+        launches += 2 + (1 if world > 1 else 0)
     else:
         launches += 1 + (1 if world > 1 else 0)
+    if args.pipeline >= 2 and world > 1:
+        launches += 2
     line = {
         "metric": "multimodal tokens/s rebalanced+dispatched+scattered per step",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -462,7 +458,9 @@ def run_ours(args):
                    "projector": projector, "d_in": list(d_in), "d_enc": list(d_enc),
                    "d_llm": d_llm, "distinct_steps": n_distinct,
                    "modality_tokens_per_step": M_total / args.steps,
-                   "planner": "pipelined on a side stream" if args.pipeline else "in-line",
+                   "planner": ("pipelined on a side stream" if args.pipeline else "in-line") +
+                              ("; dispatch of step k+1 under step k's return"
+                               if args.pipeline >= 2 else ""),
                    "balance": args.method,
                    "lssp": ({"eta": args.lssp_eta, "group": args.lssp_sp or world}
                             if args.lssp_eta >= 0 else None),

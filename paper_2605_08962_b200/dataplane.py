@@ -88,7 +88,8 @@ class MuxPath:
                  projector: bool = False, device=None, group=None, max_rows: int | None = None,
                  wait_timeout_ms: int = 20000, projector_return: str | None = None,
                  lssp_eta: int | None = None, lssp_sp: int = 1, reshard: str = "ulysses",
-                 cp_threshold: int = 0, text_embed: bool = False):
+                 cp_threshold: int = 0, text_embed: bool = False,
+                 overlap_dispatch: bool = False):
         self.capacity, self.gbs, self.dp, self.sp = capacity, gbs, dp, sp
         self.world, self.rank, self.method, self.pooled = world, rank, method, pooled
         self.d_in, self.d_enc, self.d_llm = tuple(d_in), tuple(d_enc), d_llm
@@ -120,11 +121,23 @@ class MuxPath:
         self.num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.gemm_ctas = 0  # 0: one CTA per SM; plan_ahead() leaves one SM to the planner
 
+        # overlap_dispatch: step k+1's dispatch may run under step k's return (see
+        # dispatch_overlapped); across GPUs the LLM buffers then alternate per step
+        self.overlap_dispatch = overlap_dispatch
         self.recv = [_Window(rows * d_in[g] * 2, dev, group, world) for g in range(N_GROUPS)]
-        n_llm = 2 if self.staged else 1
+        n_llm = 2 if self.staged or (overlap_dispatch and world > 1) else 1
+        self._nret = 0
         self.llm_bufs = [_Window(llm_rows * d_llm * 2, dev, group, world) for _ in range(n_llm)]
+        # completion-flag channels (each its own epoch counter): R = return and
+        # gradient exchanges, D = dispatch, E = "receive windows consumed"
         self.flags = _Window(8 * world, dev, group, world)
         self.flags.tensor.zero_()
+        self.flags_d = _Window(8 * world, dev, group, world)
+        self.flags_d.tensor.zero_()
+        self.flags_e = _Window(8 * world, dev, group, world)
+        self.flags_e.tensor.zero_()
+        self.epoch_d = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.epoch_e = torch.zeros(1, dtype=torch.int64, device=dev)
         self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
                         for g in range(N_GROUPS)]
         # copy counters x3 tables, then the projector's completion ticket
@@ -133,6 +146,7 @@ class MuxPath:
         # copy work unit and grid of the segment copies (tuning knobs; 0 = default grid)
         self.chunk_bytes = int(os.environ.get("MUX_CHUNK_BYTES", "32768"))
         self.copy_grid = int(os.environ.get("MUX_COPY_GRID", "0"))
+        self.dispatch_grid = int(os.environ.get("MUX_DISPATCH_GRID", str(self.copy_grid)))
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
@@ -140,6 +154,8 @@ class MuxPath:
         self.llm_dst = [_ptr_table(b.ptrs, dev) for b in self.llm_bufs]
         self.enc_src = _ptr_table([t.data_ptr() for t in self.enc_out], dev)
         self.flag_ptrs = _ptr_table(self.flags.ptrs, dev)
+        self.flag_ptrs_d = _ptr_table(self.flags_d.ptrs, dev)
+        self.flag_ptrs_e = _ptr_table(self.flags_e.ptrs, dev)
         self._arena_tables: dict = {}
         self._plan: Plan | None = None
         self._ring = None
@@ -258,6 +274,62 @@ class MuxPath:
         self._freed[slot] = self.return_scatter(p, main)
         return p
 
+    def run_pipeline(self, steps, *, encoder=None, after_step=None, kernel_events=None,
+                     start_event=None, stream=None):
+        """Run consecutive steps [(DeviceTable, arenas), ...] pipelined on `stream`.
+
+        The plan of step k+1 runs on the planner's side stream during step k;
+        with overlap_dispatch, step k+1's dispatch also runs (copy stream) under
+        step k's return, as soon as every rank signalled that step k's receive
+        windows were consumed.  encoder(k, plan, stream) runs between a step's
+        dispatch and its return (the encoder forward); after_step(k, plan,
+        stream) after the return.  kernel_events[k]: (start, end) events around
+        step k's return kernel."""
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        n, R = len(steps), self.RING
+        if not n:
+            return
+        self._ensure_ring()
+        base = getattr(self, "_kstep", 0)
+        slot = [(base + k) % R for k in range(n)]
+        ov = self.overlap_dispatch
+        self.plan_ahead(steps[0][0], slot[0], after=start_event)
+        if ov:
+            if getattr(self, "_copy", None) is None:
+                self._copy = torch.cuda.Stream(self.device)
+                self._dispatched = [_event() for _ in range(R)]
+            cs = self._copy
+            cs.wait_event(self._ready[slot[0]])
+            self.dispatch(self._ring[slot[0]], steps[0][1], cs)
+            self._dispatched[slot[0]].record(cs)
+        for k in range(n):
+            s = slot[k]
+            if k + 1 < n:
+                self.plan_ahead(steps[k + 1][0], slot[k + 1])
+            p = self._ring[s]
+            if ov:
+                main.wait_event(self._dispatched[s])
+            else:
+                main.wait_event(self._ready[s])
+                self.dispatch(p, steps[k][1], main)
+            if encoder is not None:
+                encoder(k, p, main)
+            if ov:
+                self.signal_consumed(main)
+                if k + 1 < n:
+                    ev = _event()
+                    ev.record(main)
+                    cs.wait_event(self._ready[slot[k + 1]])
+                    self.dispatch_overlapped(self._ring[slot[k + 1]], steps[k + 1][1], cs,
+                                             after=ev)
+                    self._dispatched[slot[k + 1]].record(cs)
+            self.kernel_events = kernel_events[k] if kernel_events else None
+            self._freed[s] = self.return_scatter(p, main)
+            self.kernel_events = None
+            if after_step is not None:
+                after_step(k, p, main)
+        self._kstep = base + n
+
     def _arena_table(self, arenas) -> torch.Tensor:
         """Device table of loader-arena pointers, cached per arena set (no sync
         once warm)."""
@@ -278,26 +350,54 @@ class MuxPath:
             ke[0].record(stream if stream is not None else torch.cuda.current_stream(self.device))
         if self.world == 1:
             _lib.check(L.mux_segcopy(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
-                                     dst.data_ptr(), self.copy_grid,
+                                     dst.data_ptr(),
+                                     self.dispatch_grid if which == 0 else self.copy_grid,
                                      self.sync[2 * which:].data_ptr(), s), "mux_segcopy")
             if ke is not None:
                 ke[1].record(stream if stream is not None else
                              torch.cuda.current_stream(self.device))
             return
         # beside an overlapped projector (which holds shared memory) copy CTAs stay lean
-        grid = -2 * self.num_sms if self.staged else self.copy_grid
+        grid = -2 * self.num_sms if self.staged else \
+            (self.dispatch_grid if which == 0 else self.copy_grid)
+        fptrs, flags, epoch = (self.flag_ptrs_d, self.flags_d, self.epoch_d) if which == 0 else \
+            (self.flag_ptrs, self.flags, self.epoch_ctr)
         _lib.check(L.mux_segcopy_ex(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
-                                    dst.data_ptr(), grid, -1, self.flag_ptrs.data_ptr(),
-                                    self.sync[2 * which:].data_ptr(), self.epoch_ctr.data_ptr(),
+                                    dst.data_ptr(), grid, -1, fptrs.data_ptr(),
+                                    self.sync[2 * which:].data_ptr(), epoch.data_ptr(),
                                     s), "mux_segcopy_ex")
         if ke is not None:
             ke[1].record(stream if stream is not None else torch.cuda.current_stream(self.device))
-        _lib.check(L.mux_wait(self.world, self.flags.tensor.data_ptr(), self.epoch_ctr.data_ptr(),
+        _lib.check(L.mux_wait(self.world, flags.tensor.data_ptr(), epoch.data_ptr(),
                               self.timeout_ms, self.wait_err.data_ptr(), s), "mux_wait")
 
     def dispatch(self, plan: Plan, arenas, stream=None):
         """Pack + dispatch: loader rows of every group to their encoder rank."""
         self._exchange(plan, 0, self._arena_table(arenas), self.recv_dst, stream)
+
+    def signal_consumed(self, stream=None):
+        """This rank's encoder has read its receive windows (E channel): peers may
+        push the next step's rows (dispatch_overlapped)."""
+        if self.world > 1:
+            _lib.check(_lib.lib().mux_signal(self.rank, self.world, self.flag_ptrs_e.data_ptr(),
+                                             self.epoch_e.data_ptr(), _stream_ptr(stream)),
+                       "mux_signal")
+
+    def dispatch_overlapped(self, plan: Plan, arenas, stream, after=None):
+        """The next step's dispatch on its own `stream`, under the current step's
+        return: waits (on `stream`) for `after` (this rank's signal_consumed) and
+        for every peer's signal_consumed, then pushes.  Needs overlap_dispatch=True
+        (alternating LLM buffers keep the returns of consecutive steps apart)."""
+        if not self.overlap_dispatch:
+            raise ValueError("MuxPath(overlap_dispatch=True) is needed")
+        if after is not None:
+            stream.wait_event(after)
+        if self.world > 1:
+            _lib.check(_lib.lib().mux_wait(self.world, self.flags_e.tensor.data_ptr(),
+                                           self.epoch_e.data_ptr(), self.timeout_ms,
+                                           self.wait_err.data_ptr(), _stream_ptr(stream)),
+                       "mux_wait")
+        self.dispatch(plan, arenas, stream)
 
     def encode_standin(self, plan: Plan, dtab: DeviceTable, stream=None):
         """Deterministic encoder stand-in E(id, t, c) into the encoder output."""
@@ -314,8 +414,11 @@ class MuxPath:
         LLM rows are final.  No host synchronisation: row counts come from the
         plan header on the device."""
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if not self.staged:  # alternate LLM buffers when there are two
+            self.last_llm = self._nret % len(self.llm_bufs)
+            self._nret += 1
         if not self.projector:
-            self._exchange(plan, 1, self.enc_src, self.llm_dst[0], main)
+            self._exchange(plan, 1, self.enc_src, self.llm_dst[self.last_llm], main)
         elif self.staged:
             return self._return_staged(plan, main)
         else:
@@ -359,11 +462,13 @@ class MuxPath:
             ke[0].record(main)
         if self.world == 1:
             _lib.check(L.mux_proj_scatter_grouped(groups, n, self.d_llm,
-                                                  self.llm_dst[0].data_ptr(), self.gemm_ctas, s),
+                                                  self.llm_dst[self.last_llm].data_ptr(),
+                                                  self.gemm_ctas, s),
                        "mux_proj_scatter_grouped")
         else:  # the GEMM's last CTA signals every peer
             _lib.check(L.mux_proj_scatter_grouped_signal(
-                groups, n, self.d_llm, self.llm_dst[0].data_ptr(), self.gemm_ctas, self.rank,
+                groups, n, self.d_llm, self.llm_dst[self.last_llm].data_ptr(), self.gemm_ctas,
+                self.rank,
                 self.world, self.flag_ptrs.data_ptr(), self.sync[6:].data_ptr(),
                 self.epoch_ctr.data_ptr(), s), "mux_proj_scatter_grouped_signal")
         if ke is not None:

@@ -87,8 +87,11 @@ def main():
                               path.llm_dst[0].data_ptr(), 0, path.sync[2:].data_ptr(), s)
                 marks.append(("return copy", ev()))
             else:
+                dst = path.llm_dst[0]
+                if os.environ.get("MUX_TIMELINE_LOCAL"):  # experiment: every row stays local
+                    dst = torch.full_like(dst, int(path.llm_bufs[0].ptrs[rank]))
                 L.mux_segcopy_signal(C.byref(p.cfg), p.ptr, 1, path.enc_src.data_ptr(),
-                                     path.llm_dst[0].data_ptr(), 0, path.flag_ptrs.data_ptr(),
+                                     dst.data_ptr(), 0, path.flag_ptrs.data_ptr(),
                                      path.sync[2:].data_ptr(), path.epoch_ctr.data_ptr(), s)
                 marks.append(("return copy", ev()))
                 L.mux_wait(world, path.flags.tensor.data_ptr(), path.epoch_ctr.data_ptr(), 20000,

@@ -33,12 +33,79 @@ def payload(rows, width, seed):
     return torch.randn(max(rows, 1), width, generator=g).to(torch.bfloat16)
 
 
+def run_overlapped(path, name, cfg, world, rank, dev, gbs, dp, sp, d_in, d_llm):
+    """MuxPath.run_pipeline with overlap_dispatch: step k+1's dispatch under step
+    k's return, 4 chained steps; each step's receive windows (captured in the
+    encoder slot) and LLM buffer checked bit-exactly.  Returns failures."""
+    descs = owork.descs_from_config(configs.DATASETS, cfg["datasets"])
+    carry, seen, steps, oracle = None, {}, [], []
+    for step in range(4):
+        _, rest, drawn, chunks = owork.generate(descs, cfg["phases"], False, step, cfg["seed"],
+                                                gbs, dp, 1, configs.CAPACITY,
+                                                carry if cfg["carry"] else None)
+        for s in drawn:
+            seen[s[0]] = s[1]
+        t = oplan.step_table(list(carry or []) if cfg["carry"] else [], drawn, chunks, seen)
+        carry = rest
+        o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, path.method)
+        arenas = [[payload(int(o["arena_rows"][r, g]), d_in[g], 7000 + 100 * step + 10 * r + g)
+                   for g in range(2)] for r in range(world)]
+        table = planner.StepTable(t["lens"].astype(np.int32), t["mods"].astype(np.int32),
+                                  t["ids"], t["carry_seq"].astype(np.int32),
+                                  t["n_carry_seqs"], np.asarray(t["chunk_off"], np.int32))
+        steps.append((planner.DeviceTable(table, dev), [a.to(dev) for a in arenas[rank]]))
+        oracle.append((t, o, arenas))
+    recv_got, llm_got = [], []
+
+    def encoder(k, p, s):
+        o = oracle[k][1]
+        recv_got.append([path.recv_view(g, int(o["recv_rows"][rank, g])).clone()
+                         for g in range(2)])
+        path.encode_standin(p, steps[k][0], s)
+
+    def after(k, p, s):
+        path.check_wait()
+        llm_got.append(path.llm_view(int(oracle[k][1]["llm_rows"][rank])).clone())
+
+    path.zero_llm()
+    torch.cuda.synchronize()
+    dist.barrier()
+    path.run_pipeline(steps, encoder=encoder, after_step=after)
+    path.finish()
+    torch.cuda.synchronize()
+    fails = 0
+    for k, (t, o, arenas) in enumerate(oracle):
+        ar = [[a.view(torch.int16).numpy().view(np.uint16) for a in arenas[r]]
+              for r in range(world)]
+        recv, _, llm = odp.run_world(o, t, world, ar, d_in, (d_llm, d_llm), d_llm)
+        for g in range(2):
+            got = recv_got[k][g].cpu().view(torch.int16).numpy().view(np.uint16)
+            if not np.array_equal(got, recv[rank][g]):
+                print(f"rank {rank} overlapped step {k}: recv group {g} differs", flush=True)
+                fails += 1
+        # LLM buffers alternate between steps and are not cleared: compare the rows
+        # this step writes (text rows are not part of the return)
+        got = llm_got[k].cpu().view(torch.int16).numpy().view(np.uint16)
+        mask = np.zeros(len(got), bool)
+        for (i, src, dst_rank, dst_row, rows) in o["pieces"]:
+            if dst_rank == rank:
+                mask[dst_row:dst_row + rows] = True
+        if not np.array_equal(got[mask], llm[rank][mask]):
+            print(f"rank {rank} overlapped step {k}: llm rows differ", flush=True)
+            fails += 1
+        if rank == 0:
+            print(f"overlapped step {k}: {int(o['recv_rows'].sum())} modality tokens ok="
+                  f"{fails == 0}", flush=True)
+    return fails
+
+
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
     narrow = "narrow" in sys.argv
     proj = "proj" in sys.argv
     lssp = "lssp" in sys.argv  # LSSP eta split: long samples sharded over encoder groups
     cp = "cp" in sys.argv  # CpHybrid LLM placement instead of Ulysses shards
+    overlap = "overlap" in sys.argv  # run_pipeline with the overlapped dispatch
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -61,7 +128,15 @@ def main():
                    projector=proj,
                    projector_return="staged" if "staged" in sys.argv else "fused",
                    lssp_eta=2048 if lssp else None, lssp_sp=world if lssp else 1,
-                   reshard="cp_hybrid" if cp else "ulysses", cp_threshold=2048 if cp else 0)
+                   reshard="cp_hybrid" if cp else "ulysses", cp_threshold=2048 if cp else 0,
+                   overlap_dispatch=overlap)
+    if overlap:
+        path.method = "lpt_local"
+        fails = run_overlapped(path, name, cfg, world, rank, dev, gbs, dp, sp, d_in, d_llm)
+        t = torch.tensor([fails], device=dev)
+        dist.all_reduce(t)
+        dist.destroy_process_group()
+        sys.exit(1 if int(t.item()) else 0)
     if proj:
         gw = torch.Generator().manual_seed(9)
         Ws = [(torch.randn(d_llm, d_enc[g], generator=gw) / d_enc[g] ** 0.5).to(torch.bfloat16)

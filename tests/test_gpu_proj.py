@@ -172,9 +172,12 @@ def test_step_with_projector_matches_oracle(cuda_device, name, step):
     raise AssertionError(f"{name} golden step {step} missing")
 
 
-def test_pipelined_ring_matches_oracle(cuda_device):
-    """The bench's pipelined form: step k+1 planned on the side stream (plan ring,
-    row map built there) while step k moves; every step's LLM rows checked."""
+@pytest.mark.parametrize("overlap", [False, True])
+def test_pipelined_ring_matches_oracle(cuda_device, overlap):
+    """The bench's pipelined form (MuxPath.run_pipeline): step k+1 planned on the
+    side stream (plan ring, row map built there) while step k moves, and with
+    overlap_dispatch its dispatch on the copy stream under step k's projector;
+    every step's LLM rows checked."""
     from oracle import planner as oplan
     from paper_2605_08962_b200 import configs, planner
     from paper_2605_08962_b200.dataplane import MuxPath
@@ -186,7 +189,7 @@ def test_pipelined_ring_matches_oracle(cuda_device):
     cap, gbs = configs.CAPACITY, steps[0][0]["gbs"]
     d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, 512
     path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_enc=d_enc, d_llm=d_llm,
-                   projector=True, method="lpt_local")
+                   projector=True, method="lpt_local", overlap_dispatch=overlap)
     g = torch.Generator().manual_seed(5)
     Ws = [(torch.randn(d_llm, d_enc[k], generator=g) / d_enc[k] ** 0.5).to(torch.bfloat16).cuda()
           for k in range(2)]
@@ -196,17 +199,16 @@ def test_pipelined_ring_matches_oracle(cuda_device):
     os_ = [oplan.plan_step(t, cap, gbs, 1, 1, 1, 1, "lpt_local") for _, t in steps]
     arenas = [[torch.zeros(max(int(o["arena_rows"][0, k]), 1), d_in[k], dtype=torch.bfloat16,
                            device="cuda") for k in range(2)] for o in os_]
-    R = path.RING
     outs = []
-    path.plan_ahead(tabs[0], 0)
-    for k in range(len(steps)):
-        if k + 1 < len(steps):
-            path.plan_ahead(tabs[k + 1], (k + 1) % R)
+
+    def encoder(k, p, s):
         path.llm_view().zero_()
-        path.run_planned(k % R, arenas[k],
-                         encoder=lambda p, s, k=k: path.encode_standin(p, tabs[k], s))
-        n = int(os_[k]["llm_rows"][0])
-        outs.append(path.llm_view(n).float().clone())
+        path.encode_standin(p, tabs[k], s)
+
+    def after(k, p, s):
+        outs.append(path.llm_view(int(os_[k]["llm_rows"][0])).float().clone())
+
+    path.run_pipeline(list(zip(tabs, arenas)), encoder=encoder, after_step=after)
     torch.cuda.synchronize()
     from oracle import dataplane as odp
     for k, ((st, t), o) in enumerate(zip(steps, os_)):
