@@ -677,7 +677,8 @@ def cpu_baseline(name, table, projector, world=1, method="lpt_local"):
               "oracle planner + torch-CPU gather/scatter"
               + (f"; projector timed on 4096 rows, x{scale:.1f} extrapolated" if projector else ""))
     return {"value": M / total, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": sample, "seconds": {"plan": t_plan, "pack": t_pack, "return": t_ret}}
+            "sample": sample, "seconds": {"plan": t_plan, "pack": t_pack, "return": t_ret},
+            "step_seconds": total}
 
 
 def run_reference(args):
@@ -699,7 +700,9 @@ def run_reference(args):
     v = float(np.mean([r["value"] for r in vals]))
     line = {"metric": "multimodal tokens/s rebalanced+dispatched+scattered per step",
             "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup,
+            "ms_per_step": float(np.mean([r["step_seconds"] for r in vals])) * 1e3,
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": name, "global_batch": gbs, "seq_len": configs.CAPACITY,
