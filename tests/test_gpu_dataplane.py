@@ -196,3 +196,37 @@ def test_dataplane_with_text_rows(cuda_device):
 def _lib_H_TEXT_ROWS():
     from paper_2605_08962_b200 import _lib
     return _lib.H_TEXT_ROWS
+
+
+def test_all_text_step_moves_no_modality_rows(cuda_device):
+    """A step with text samples only: no dispatch, no return, the projector GEMM
+    sees M = 0 on the device; the text rows are still gathered."""
+    lens = np.array([4000, 3000, 9000, 120, 0, 5000])
+    t = dict(lens=lens, mods=np.zeros(len(lens), np.int64), ids=np.arange(10, 10 + len(lens)),
+             carry_seq=np.zeros(0, np.int64), n_carry_seqs=0, chunk_off=[0, len(lens)])
+    o = oplan.plan_step(t, configs.CAPACITY, 1, 1, 1, 1, 1, "lpt")
+    assert int(o["recv_rows"].sum()) == 0 and not o["pieces"]
+    path = MuxPath(capacity=configs.CAPACITY, gbs=1, dp=1, d_in=(20, 8), d_enc=(256, 256),
+                   d_llm=256, projector=True, text_embed=True)
+    for g in range(2):
+        path.set_projector(g, torch.randn(256, 256, device="cuda").to(torch.bfloat16))
+    table = to_table(t)
+    dtab = planner.DeviceTable(table, "cuda")
+    plan = path.plan(dtab)
+    h = plan.check(table)
+    assert int(h[3]) == 0 and int(h[4]) == 0  # no dispatch segments, no return pieces
+    path.llm_view().zero_()
+    path.dispatch(plan, [torch.zeros(1, 20, dtype=torch.bfloat16, device="cuda"),
+                         torch.zeros(1, 8, dtype=torch.bfloat16, device="cuda")])
+    path.return_scatter(plan)
+    emb = payload(100, 256, 3)
+    tokens = torch.randint(0, 100, (int(lens.sum()),), dtype=torch.int32)
+    path.embed_text(plan, tokens.cuda(), emb.cuda())
+    torch.cuda.synchronize()
+    path.check_text()
+    n = int(o["llm_rows"][0])
+    llm = [np.zeros((n, 256), np.uint16)]
+    llm = odp.run_text(o, t, 1, tokens.numpy(), emb.view(torch.int16).numpy().view(np.uint16),
+                       llm)
+    got = path.llm_view(n).cpu().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, llm[0])

@@ -377,3 +377,22 @@ def test_text_segments_match_oracle(cuda_device, reshard):
                 assert np.array_equal(d["rseg"], odp.pieces_by_rank(o, me))
                 n += 1
     assert n > 20
+
+
+def test_plan_at_the_sample_limit(cuda_device):
+    """4096 samples (the device planner's limit) plan bit-exactly; 4097 is refused
+    with a ValueError before any launch."""
+    rs = np.random.RandomState(8)
+    n = 4096
+    lens = rs.randint(1, 600, size=n)
+    t = dict(lens=lens, mods=rs.randint(0, 4, size=n), ids=rs.permutation(n),
+             carry_seq=np.zeros(0, np.int64), n_carry_seqs=0,
+             chunk_off=[0, 1500, 3000, n])
+    o = oplan.plan_step(t, 16384, 8, 8, 1, 8, 1, "lpt")
+    for me in (0, 7):
+        d = device_plan(t, 16384, 8, 8, 1, 8, me, "lpt")
+        assert_plan_equal(d, o, t, me)
+    t2 = dict(t, lens=np.append(lens, 5), mods=np.append(t["mods"], 1),
+              ids=np.append(t["ids"], n), chunk_off=[0, 1500, 3000, n + 1])
+    with pytest.raises(ValueError, match="4096"):
+        device_plan(t2, 16384, 8, 8, 1, 8, 0, "lpt")
