@@ -261,19 +261,6 @@ class MuxPath:
         self._ready[slot].record(side)
         return p
 
-    def run_planned(self, slot: int, arenas, stream=None, encoder=None) -> Plan:
-        """Dispatch + return of the plan in ring `slot` on the main stream.
-        `encoder(plan, stream)`, if given, runs between them (the encoder
-        forward: receive windows in, `enc_out` rows out)."""
-        main = stream if stream is not None else torch.cuda.current_stream(self.device)
-        main.wait_event(self._ready[slot])
-        p = self._ring[slot]
-        self.dispatch(p, arenas, main)
-        if encoder is not None:
-            encoder(p, main)
-        self._freed[slot] = self.return_scatter(p, main)
-        return p
-
     def run_pipeline(self, steps, *, encoder=None, after_step=None, kernel_events=None,
                      start_event=None, stream=None):
         """Run consecutive steps [(DeviceTable, arenas), ...] pipelined on `stream`.
