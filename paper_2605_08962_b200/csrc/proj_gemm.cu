@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "mux_common.cuh"
@@ -306,6 +307,223 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- CTA-pair variant (cta_group::2; the default, MUX_GEMM_2CTA=0 selects the
+// single-CTA kernel above) ------------------------------------------------------
+// A cluster of two CTAs on one TPC computes 256 x 256 output tiles with
+// tcgen05.mma.cta_group::2 (M256 N256 K16) issued by the leader: each CTA
+// stages its 128-row half of A and its 128-column half of B, so a stage is
+// 32 KB instead of 48 KB and the ring is 6 deep; both CTAs' TMA loads
+// complete on the leader's full barrier; the MMA commits multicast to both
+// CTAs' empty/tfull barriers; each CTA drains its own 128 TMEM lanes and
+// arrives on the leader's tempty barrier.
+constexpr int BM2 = 256, STAGES2 = 6;
+constexpr int A2_BYTES = 128 * BK * 2;
+constexpr int B2_BYTES = 128 * BK * 2;
+constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr int kSmem2 = STAGES2 * STAGE2_BYTES + 256 + kStagingBytes + 1024;
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    proj_scatter_pair_kernel(const __grid_constant__ GroupParams P) {
+  using namespace umma;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t cid = cluster_id_x(), ncl = n_clusters_x();
+  const int N = P.N, num_n = N / BN, G = P.n_groups;
+  TileMap tm;
+  tm.tiles[0] = 0;
+  for (int g = 0; g < G; ++g) {
+    int64_t M = P.M_max[g];
+    if (P.M_dev[g]) {
+      const int64_t m = *P.M_dev[g];
+      M = m < M ? (m > 0 ? m : 0) : M;
+    }
+    tm.M[g] = M;
+    tm.kblocks[g] = P.K[g] / BK;
+    tm.num_m[g] = (int)((M + BM2 - 1) / BM2);
+    tm.stride[g] = block_stride(tm.num_m[g]);
+    tm.tiles[g + 1] = tm.tiles[g] + (int64_t)tm.num_m[g] * num_n;
+  }
+  const int64_t num_tiles = tm.tiles[G];
+
+  if (warp == 0 && lane == 0) {
+    for (int g = 0; g < G; ++g) {
+      tma_prefetch(&P.ta[g]);
+      tma_prefetch(&P.tb[g]);
+    }
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);  // one arrival per epilogue warp of each CTA
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+        int g, m_blk, n_blk;
+        locate(tm, G, num_n, tile, g, m_blk, n_blk);
+        for (int kb = 0; kb < tm.kblocks[g]; ++kb) {
+          mbar_wait_bounded(&empty[stage], phase ^ 1, true);
+          uint8_t* sa = smem + stage * STAGE2_BYTES;
+          if (leader) mbar_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+          const uint32_t bar = smem_u32(&full[stage]) & kPeerBitMask;
+          tma_load_2d_pair(sa, &P.ta[g], bar, kb * BK, m_blk * BM2 + (int)rank * 128, pol);
+          tma_load_2d_pair(sa + A2_BYTES, &P.tb[g], bar, kb * BK, n_blk * BN + (int)rank * 128,
+                           pol);
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM2, BN);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+        int g, m_blk, n_blk;
+        locate(tm, G, num_n, tile, g, m_blk, n_blk);
+        mbar_wait_bounded(&tempty[acc], acc_phase ^ 1, true);
+        fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < tm.kblocks[g]; ++kb) {
+          mbar_wait_bounded(&full[stage], phase, false);
+          fence_after();
+          const uint8_t* sa = smem + stage * STAGE2_BYTES;
+          const uint64_t ad = sdesc_sw128(sa), bd = sdesc_sw128(sa + A2_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int quarter = warp & 3, colgrp = (warp - 2) >> 2;
+    uint4* stage = reinterpret_cast<uint4*>(smem + STAGES2 * STAGE2_BYTES + 256) +
+                   (warp - 2) * (32 * 8);
+    const uint32_t tempty_leader[2] = {mapa(smem_u32(&tempty[0]), 0),
+                                       mapa(smem_u32(&tempty[1]), 0)};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+      int g, m_blk, n_blk;
+      locate(tm, G, num_n, tile, g, m_blk, n_blk);
+      const uint16_t* bias = P.bias[g];
+      const int64_t m = (int64_t)m_blk * BM2 + (int)rank * 128 + quarter * 32 + lane;
+      char* my_dst = nullptr;
+      if (m < tm.M[g]) {
+        const int64_t rd = P.row_dst[g][m];
+        my_dst = static_cast<char*>(P.out_bases[rd >> 40]) +
+                 ((rd & kRowMask) * N + (int64_t)n_blk * BN + colgrp * 128) * 2;
+      }
+      mbar_wait_bounded(&tfull[acc], acc_phase, true);
+      fence_after();
+#pragma unroll 1
+      for (int sub = 0; sub < 2; ++sub) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          uint32_t v[32];
+          const int col = colgrp * 128 + sub * 64 + j * 32;
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + col, v);
+          tmem_wait_ld();
+          const int n0 = n_blk * BN + col;
+          uint32_t o[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            float x0 = __uint_as_float(v[2 * c]), x1 = __uint_as_float(v[2 * c + 1]);
+            if (bias) {
+              const uint32_t bb = __ldg(reinterpret_cast<const uint32_t*>(bias + n0 + 2 * c));
+              x0 += __uint_as_float(bb << 16);
+              x1 += __uint_as_float(bb & 0xffff0000u);
+            }
+            o[c] = pack_bf16(x0, x1);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            stage[lane * 8 + ((j * 4 + q) ^ (lane & 7))] =
+                make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        }
+        __syncwarp();
+        const int c8 = lane & 7;
+#pragma unroll 4
+        for (int r = 0; r < 32; r += 4) {
+          const int row = r + (lane >> 3);
+          char* dd = reinterpret_cast<char*>(__shfl_sync(MUX_FULL, (unsigned long long)my_dst, row));
+          const uint4 val = stage[row * 8 + (c8 ^ (row & 7))];
+          if (dd) *reinterpret_cast<uint4*>(dd + sub * 128 + c8 * 16) = val;
+        }
+        __syncwarp();
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  fence_before();
+  if (P.world > 0) __threadfence_system();
+  __syncthreads();
+  cluster_sync();  // the peer's MMAs (issued by the leader) are done with this TMEM
+  fence_after();
+  if (warp == 1) tmem_free_pair<512>(tmem_base);
+  if (P.world > 0 && warp == 0) {
+    __shared__ bool s_last;
+    if (lane == 0) s_last = atomicAdd(P.ticket, 1u) == gridDim.x - 1;
+    __syncwarp();
+    if (s_last) {
+      const uint64_t e = *P.epoch_ctr + 1;
+      __syncwarp();
+      if (lane == 0) {
+        *P.ticket = 0;
+        *P.epoch_ctr = e;
+      }
+      __threadfence_system();
+      if (lane < P.world) {
+        uint64_t* f = P.flags_peers[lane] + P.me;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+      }
+    }
+  }
+}
+
 // --- host: tensor maps through the driver entry point (no -lcuda link) --------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -391,6 +609,7 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
   P.N = N;
   P.out_bases = out_bases;
   int64_t tiles = 0;
+  const uint16_t* groups_W[kMaxGroups] = {nullptr, nullptr};
   for (int i = 0; i < n_groups; ++i) {
     const mux_proj_group& q = groups[i];
     if (q.K % BK || q.K <= 0 || q.M_max < 0) {
@@ -405,6 +624,7 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
     st = make_map(&P.tb[g], q.W, N, q.K, BN);
     if (st) return st;
     P.bias[g] = q.bias;
+    groups_W[g] = q.W;
     P.row_dst[g] = q.row_dst;
     P.M_dev[g] = q.M_dev;
     P.M_max[g] = q.M_max;
@@ -419,6 +639,48 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
   if (P.n_groups == 0) {
     // nothing to compute: still publish the epoch (peers wait for it)
     return world > 0 ? mux_signal(me, world, flags_peers, epoch_ctr, stream) : MUX_OK;
+  }
+  static int pair = -1;  // the CTA-pair (cta_group::2) kernel unless MUX_GEMM_2CTA=0
+  if (pair < 0) {
+    const char* e = getenv("MUX_GEMM_2CTA");
+    pair = e ? atoi(e) : 1;
+  }
+  if (pair) {
+    // B maps with 128-row boxes (each CTA stages half of the 256-column tile)
+    for (int g = 0; g < P.n_groups; ++g) {
+      int st = make_map(&P.tb[g], groups_W[g], N, P.K[g], 128);
+      if (st) return st;
+    }
+    static bool attr2 = false;
+    if (!attr2) {
+      MUX_CUDA(cudaFuncSetAttribute(proj_scatter_pair_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
+      attr2 = true;
+    }
+    int sms = num_sms;
+    if (sms <= 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int64_t tiles2 = 0;
+    for (int g = 0; g < P.n_groups; ++g) tiles2 += ((P.M_max[g] + BM2 - 1) / BM2) * (N / BN);
+    int pairs = sms / 2;
+    if (tiles2 < pairs) pairs = (int)tiles2;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(2 * pairs);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = kSmem2;
+    lc.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    MUX_CUDA(cudaLaunchKernelEx(&lc, proj_scatter_pair_kernel, P));
+    return MUX_OK;
   }
   static bool attr = false;
   if (!attr) {
