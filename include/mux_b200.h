@@ -16,7 +16,11 @@
  *                        + build_global_batch (:265-278) + replica slicing
  *                        (:177-180) + balance.grouped_reorder / kk_partition
  *                         + reshard.plan_reshard UlyssesUniform
- *                        (SPEC.md:462-470), fused into one device plan.
+ *                        (SPEC.md:462-470), fused into one device plan; with
+ *                        cfg.reshard = CpHybrid, plan_reshard's CpHybrid variant
+ *                        (SPEC.md:456-469, :497); with cfg.lssp_sp, the LSSP
+ *                        eta split of lssp_schedule; with
+ *                        cfg.text_embed, the text rows' segment table.
  *   mux_assign           balance.kk_partition and the LPT
  *                        greedy named by BASELINE.json north_star.
  *   mux_segcopy          the data all-to-all of grouped_reorder
@@ -24,8 +28,12 @@
  *                        pack, dispatch, return and scatter are all segment
  *                        copies over local or NVLink-peer pointers.
  *   mux_signal/mux_wait  cross-GPU completion flags for the push exchange.
- *   mux_proj_scatter     projector GEMM fused with the placeholder scatter
- *                        (no reference code, adapter).
+ *   mux_proj_scatter*    projector GEMM fused with the placeholder scatter
+ *                        (no reference code, adapter); the
+ *                        grouped forms run both encoder groups in one launch
+ *                        and can fuse the completion signal.
+ *   mux_text_embed       the LLM embedding rows of the text tokens in the same
+ *                        packed buffer.
  *   mux_encoder_standin  deterministic stand-in for the (out of scope) encoder.
  */
 #ifndef MUX_B200_H
