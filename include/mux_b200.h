@@ -181,6 +181,9 @@ typedef struct {
 } mux_plan_layout;
 
 int mux_version(void);
+/* sizeof(mux_plan_cfg), sizeof(mux_plan_layout), sizeof(mux_proj_group) into
+ * out[0..2]: lets a binding check its struct mirrors against this build. */
+void mux_abi_sizes(int64_t* out);
 const char* mux_last_error(void);
 
 /* Layout of the plan buffer for `cfg`; returns MUX_OK or MUX_ERR_VALUE. */

@@ -67,6 +67,7 @@ class ProjGroup(C.Structure):
 _P = C.c_void_p
 _SIGS = [
     ("mux_version", C.c_int, []),
+    ("mux_abi_sizes", None, [_P]),
     ("mux_last_error", C.c_char_p, []),
     ("mux_plan_layout_of", C.c_int, [C.POINTER(PlanCfg), C.POINTER(PlanLayout)]),
     ("mux_plan_step", C.c_int, [C.POINTER(PlanCfg), _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),

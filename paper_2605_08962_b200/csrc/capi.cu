@@ -22,5 +22,11 @@ int cuda_status(cudaError_t e, const char* where) {
 
 }  // namespace mux
 
-extern "C" int mux_version(void) { return 1; }
+extern "C" int mux_version(void) { return 2; }
+
+extern "C" void mux_abi_sizes(int64_t* out) {
+  out[0] = (int64_t)sizeof(mux_plan_cfg);
+  out[1] = (int64_t)sizeof(mux_plan_layout);
+  out[2] = (int64_t)sizeof(mux_proj_group);
+}
 extern "C" const char* mux_last_error(void) { return mux::g_err; }

@@ -7,7 +7,7 @@ import re
 import numpy as np
 import pytest
 
-from paper_2605_08962_b200 import configs, workload as W
+from paper_2605_08962_b200 import _lib, configs, workload as W
 from tests.helpers import golden
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -99,13 +99,13 @@ def test_export_batch_matches_reference_bytes(tmp_path):
 def test_capi_exports_every_declared_symbol():
     from paper_2605_08962_b200 import _lib
     hdr = open(os.path.join(ROOT, "include", "mux_b200.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|const char\*|size_t)\s+(mux_\w+)\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:int|void|const char\*|size_t)\s+(mux_\w+)\(", hdr, re.M))
     assert declared, "no declarations parsed"
     L = _lib.lib()
     for name in declared:
         assert hasattr(L, name), name
     assert declared == set(_lib.EXPORTS)
-    assert L.mux_version() == 1
+    assert L.mux_version() == 2
 
 
 def test_plan_layout_on_cpu():
@@ -119,3 +119,13 @@ def test_plan_layout_on_cpu():
     cfg.S = 100000
     with pytest.raises(ValueError):
         planner.layout_of(cfg)
+
+
+def test_ctypes_struct_mirrors_match_the_library():
+    """The ctypes mirrors of mux_plan_cfg / mux_plan_layout / mux_proj_group have
+    the C sizes (no GPU needed: mux_abi_sizes is host code)."""
+    import ctypes as C
+    out = (C.c_int64 * 3)()
+    _lib.lib().mux_abi_sizes(out)
+    assert list(out) == [C.sizeof(_lib.PlanCfg), C.sizeof(_lib.PlanLayout),
+                         C.sizeof(_lib.ProjGroup)]
