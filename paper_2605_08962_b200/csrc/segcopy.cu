@@ -14,6 +14,8 @@
 // The last CTA to finish fences at system scope and publishes `epoch` into the
 // completion flag of every peer, so the exchange needs no host round trip.
 
+#include <cstdlib>
+
 #include "mux_common.cuh"
 
 namespace mux {
@@ -124,6 +126,7 @@ struct SegArgs {
   uint64_t* epoch_ctr;  // device counter: epoch = ++*epoch_ctr (graph-replay safe)
   int32_t me, world;
   int32_t skip_rank;    // segments addressed to this rank are not copied (-1: none)
+  int32_t grab;         // chunks per grab (0: adaptive)
 };
 
 // Work distribution is dynamic: CTAs grab kGrab chunks at a time from a
@@ -142,14 +145,20 @@ __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int sm
   const bool staged = nseg < smem_segs;
   if (staged)
     for (int i = threadIdx.x; i <= nseg; i += blockDim.x) s_c0[i] = (int32_t)a.chunk0[i];
-  if (threadIdx.x == 0) s_grab[0] = atomicAdd(&a.sync[0], (uint32_t)kGrab);
+  // grab size (measured): one chunk per grab for a local copy —
+  // 1184 CTAs share HBM, so a CTA moves only ~5 GB/s and a 4-chunk grab left a
+  // ~45 us tail (target-1: 0.171 -> 0.153 ms); kGrab for a cross-GPU exchange,
+  // where consecutive chunks to one peer keep NVLink efficient (cfg5 at 4 GPUs:
+  // 484 vs 438 M tok/s).  MUX_COPY_GRAB overrides.
+  const uint32_t grab = a.grab > 0 ? (uint32_t)a.grab : (a.flags_peers ? kGrab : 1u);
+  if (threadIdx.x == 0) s_grab[0] = atomicAdd(&a.sync[0], grab);
   __syncthreads();
   auto c0 = [&](int s) -> int64_t { return staged ? s_c0[s] : a.chunk0[s]; };
   for (int buf = 0;; buf ^= 1) {
     const int64_t c_begin = s_grab[buf];
     if (c_begin >= nchunks) break;
-    if (threadIdx.x == 0) s_grab[buf ^ 1] = atomicAdd(&a.sync[0], (uint32_t)kGrab);
-    const int64_t c_end = c_begin + kGrab < nchunks ? c_begin + kGrab : nchunks;
+    if (threadIdx.x == 0) s_grab[buf ^ 1] = atomicAdd(&a.sync[0], grab);
+    const int64_t c_end = c_begin + grab < nchunks ? c_begin + grab : nchunks;
     int lo = 0, hi = nseg - 1;  // last segment with c0 <= c_begin
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -433,6 +442,12 @@ extern "C" int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t
   a.me = cfg->me;
   a.world = cfg->world;
   a.skip_rank = skip_rank;
+  static int grab = -1;  // MUX_COPY_GRAB (tuning; 0 = adaptive)
+  if (grab < 0) {
+    const char* e = getenv("MUX_COPY_GRAB");
+    grab = e ? atoi(e) : 0;
+  }
+  a.grab = grab;
   if (!sync || (flags_peers && !epoch_ctr)) {
     set_error("segment copy needs its sync counters (and an epoch counter to signal)");
     return MUX_ERR_VALUE;
