@@ -35,12 +35,17 @@ def _digest(plan):
     return h.hexdigest()
 
 
-def _worker(rank, world, port, cases, result_q):
+def _worker(rank, world, port, cases, result_q, mode="plain"):
+    from oracle import cphybrid as ocph
+    from oracle import lssp as olssp
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     ok = True
     for t, st, d_in, d_llm in cases:
         plan = oplan.plan_step(t, 16384, st["gbs"], st["dp"], world // st["dp"], world)
+        if mode == "cp":
+            plan = ocph.place(plan, t, st["gbs"], st["dp"], world // st["dp"], 16384, 2048)
+        lay = olssp.layout(plan, t["lens"], world, 2048, world) if mode == "lssp" else None
         digests = [None] * world
         dist.all_gather_object(digests, _digest(plan))
         ok &= len(set(digests)) == 1  # every rank computed the identical plan
@@ -50,20 +55,28 @@ def _worker(rank, world, port, cases, result_q):
                               dtype=np.uint16) for q in range(2)] for r in range(world)]
         # dispatch: my segments, pushed as (dst rank, group, dst row, rows payload)
         sends = [[] for _ in range(world)]
-        for src, dst, n, q, to in odp.dispatch_by_rank(plan, t["lens"], rank).tolist():
+        dsegs = odp.dispatch_by_rank(plan, t["lens"], rank) if lay is None else \
+            olssp.dispatch_by_rank(plan, lay, t["lens"], rank)
+        for src, dst, n, q, to in dsegs.tolist():
             sends[to].append((q, dst, arenas[rank][q][src:src + n]))
         got = [None] * world
         dist.all_gather_object(got, sends)
-        recv = [np.zeros((int(plan["recv_rows"][rank, q]), d_in[q]), np.uint16) for q in range(2)]
+        rows_of = plan["recv_rows"] if lay is None else lay["recv_rows"]
+        recv = [np.zeros((int(rows_of[rank, q]), d_in[q]), np.uint16) for q in range(2)]
         for r in range(world):
             for q, dst, rows in got[r][rank]:
                 recv[q][dst:dst + len(rows)] = rows
-        ref_recv, enc_out, ref_llm = odp.run_world(plan, t, world, arenas, d_in, (d_llm,) * 2,
-                                                   d_llm)
+        if lay is None:
+            ref_recv, enc_out, ref_llm = odp.run_world(plan, t, world, arenas, d_in,
+                                                       (d_llm,) * 2, d_llm)
+        else:
+            ref_recv, enc_out, ref_llm = olssp.run_world(plan, lay, t, world, arenas, d_in,
+                                                         (d_llm,) * 2, d_llm)
         ok &= all(np.array_equal(recv[q], ref_recv[rank][q]) for q in range(2))
         # return: my encoder rows to their LLM ranks
         sends = [[] for _ in range(world)]
-        for src, dst, n, q, to in odp.pieces_by_rank(plan, rank).tolist():
+        rsegs = odp.pieces_by_rank(plan, rank) if lay is None else olssp.return_by_rank(lay, rank)
+        for src, dst, n, q, to in rsegs.tolist():
             sends[to].append((dst, enc_out[rank][q][src:src + n]))
         got = [None] * world
         dist.all_gather_object(got, sends)
@@ -76,17 +89,23 @@ def _worker(rank, world, port, cases, result_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_push_protocol_gloo(world):
+@pytest.mark.parametrize("world,mode", [(2, "plain"), (2, "lssp"), (2, "cp")])
+def test_push_protocol_gloo(world, mode):
+    """Plain Ulysses placement, the LSSP eta split (group = both ranks, eta 2048)
+    and CpHybrid placement (threshold 2048): each rank's segment tables alone
+    rebuild every buffer."""
     cases = []
     for name, st, t, _ in golden_steps():
         if st["world"] == world and name in ("cfg5", "cfg3") and st["step"] < 2:
+            if mode == "cp" and st["dp"] == world:
+                st = dict(st, dp=1)  # one replica, its CP group = both ranks
             cases.append((t, st, (12, 4), 16))
     assert cases
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, mode))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(world))
