@@ -274,12 +274,6 @@ int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, const int64_t
 int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_t group,
                     int64_t* row_dst, int64_t n_rows, void* stream);
 
-/* As mux_return_rows; with stage_slot >= 0 the pieces addressed to other
- * ranks map to (stage_slot << 40) | source row instead, so a projector GEMM
- * can store them locally (out_bases[stage_slot]) for a later push. */
-int mux_return_rows_ex(const mux_plan_cfg* cfg, const void* plan, int32_t group,
-                       int64_t* row_dst, int64_t n_rows, int32_t stage_slot, void* stream);
-
 /* MUX_RET_STAGED: per-row destination of the owner's staging rows of
  * `group`: row_dst[stage_off + t] = (me << 40) | (llm_row + t).  lens: the
  * step table's int32 lengths (device). */

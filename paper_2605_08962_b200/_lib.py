@@ -79,8 +79,6 @@ _SIGS = [
                                      _P, _P, _P]),
     ("mux_segcopy_ex", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, _P, C.c_int32,
                                  C.c_int32, _P, _P, _P, _P]),
-    ("mux_return_rows_ex", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, C.c_int64,
-                                     C.c_int32, _P]),
     ("mux_copy_bytes", C.c_int, [_P, _P, C.c_int64, C.c_int32, _P]),
     ("mux_memcpy_async", C.c_int, [_P, _P, C.c_int64, _P]),
     ("mux_signal", C.c_int, [C.c_int32, C.c_int32, _P, _P, _P]),

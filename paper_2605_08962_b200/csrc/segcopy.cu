@@ -315,21 +315,16 @@ __global__ void __launch_bounds__(256) standin_kernel(Plan p, int S, int me, int
 }
 
 // row_dst[src row] = (dst rank << 40) | dst row of every return piece of
-// `group`; with stage_slot >= 0, pieces for other ranks go to slot
-// `stage_slot` at their own (encoder-order) row instead, for a later push.
-__global__ void return_rows_kernel(Plan p, int group, int64_t* row_dst, int64_t n_rows, int me,
-                                   int stage_slot) {
+// `group` (group < 0: every group, group g's map at row_dst + g * n_rows).
+__global__ void return_rows_kernel(Plan p, int group, int64_t* row_dst, int64_t n_rows) {
   const int64_t npieces = p.hdr[MUX_H_N_RETURN];
   for (int64_t s = blockIdx.x; s < npieces; s += gridDim.x) {
     if (group >= 0 && p.rgroup[s] != group) continue;
-    // group < 0: every group, group g's map at row_dst + g * n_rows
     int64_t* rd = group >= 0 ? row_dst : row_dst + (int64_t)p.rgroup[s] * n_rows;
     const int64_t src = p.rsrc[s], dst = p.rdst[s], n = p.rrows[s];
-    const bool staged = stage_slot >= 0 && p.rrank[s] != me;
-    const int64_t tag = (int64_t)(staged ? stage_slot : p.rrank[s]) << 40;
-    const int64_t base = staged ? src : dst;
+    const int64_t tag = (int64_t)p.rrank[s] << 40;
     for (int64_t t = threadIdx.x; t < n; t += blockDim.x)
-      if (src + t < n_rows) rd[src + t] = tag | (base + t);
+      if (src + t < n_rows) rd[src + t] = tag | (dst + t);
   }
 }
 
@@ -503,18 +498,12 @@ extern "C" int mux_encoder_standin(const mux_plan_cfg* cfg, const void* plan, co
 
 extern "C" int mux_return_rows(const mux_plan_cfg* cfg, const void* plan, int32_t group,
                                int64_t* row_dst, int64_t n_rows, void* stream) {
-  return mux_return_rows_ex(cfg, plan, group, row_dst, n_rows, -1, stream);
-}
-
-extern "C" int mux_return_rows_ex(const mux_plan_cfg* cfg, const void* plan, int32_t group,
-                                  int64_t* row_dst, int64_t n_rows, int32_t stage_slot,
-                                  void* stream) {
   mux_plan_layout L;
   int st = mux_plan_layout_of(cfg, &L);
   if (st) return st;
   Plan p = make_plan_const(plan, L);
-  return_rows_kernel<<<256, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, group, row_dst, n_rows,
-                                                                         cfg->me, stage_slot);
+  return_rows_kernel<<<256, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, group, row_dst,
+                                                                         n_rows);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }
