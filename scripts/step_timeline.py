@@ -90,6 +90,12 @@ def main():
                 dst = path.llm_dst[0]
                 if os.environ.get("MUX_TIMELINE_LOCAL"):  # experiment: every row stays local
                     dst = torch.full_like(dst, int(path.llm_bufs[0].ptrs[rank]))
+                if os.environ.get("MUX_TIMELINE_PLAIN"):  # experiment: local, non-VMM buffer
+                    if not hasattr(path, "_plain"):
+                        path._plain = torch.empty_like(path.llm_bufs[0].tensor)
+                    dst = torch.full_like(dst, int(path._plain.data_ptr()))
+                if os.environ.get("MUX_TIMELINE_RING"):  # experiment: every row to rank+1
+                    dst = torch.full_like(dst, int(path.llm_bufs[0].ptrs[(rank + 1) % world]))
                 L.mux_segcopy_signal(C.byref(p.cfg), p.ptr, 1, path.enc_src.data_ptr(),
                                      dst.data_ptr(), 0, path.flag_ptrs.data_ptr(),
                                      path.sync[2:].data_ptr(), path.epoch_ctr.data_ptr(), s)
