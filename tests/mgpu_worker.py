@@ -33,10 +33,12 @@ def payload(rows, width, seed):
     return torch.randn(max(rows, 1), width, generator=g).to(torch.bfloat16)
 
 
-def run_overlapped(path, name, cfg, world, rank, dev, gbs, dp, sp, d_in, d_llm):
+def run_overlapped(path, name, cfg, world, rank, dev, gbs, dp, sp, d_in, d_llm, proj=None):
     """MuxPath.run_pipeline with overlap_dispatch: step k+1's dispatch under step
     k's return, 4 chained steps; each step's receive windows (captured in the
-    encoder slot) and LLM buffer checked bit-exactly.  Returns failures."""
+    encoder slot) and LLM buffer checked bit-exactly — or, with proj = (Ws, bs,
+    d_enc), the projected rows against an fp32 reference (the bench's default
+    multi-GPU path: pair GEMM, fused signal, overlapped dispatch).  Returns failures."""
     descs = owork.descs_from_config(configs.DATASETS, cfg["datasets"])
     carry, seen, steps, oracle = None, {}, [], []
     for step in range(4):
@@ -85,14 +87,31 @@ def run_overlapped(path, name, cfg, world, rank, dev, gbs, dp, sp, d_in, d_llm):
                 fails += 1
         # LLM buffers alternate between steps and are not cleared: compare the rows
         # this step writes (text rows are not part of the return)
-        got = llm_got[k].cpu().view(torch.int16).numpy().view(np.uint16)
-        mask = np.zeros(len(got), bool)
+        mask = np.zeros(int(o["llm_rows"][rank]), bool)
         for (i, src, dst_rank, dst_row, rows) in o["pieces"]:
             if dst_rank == rank:
                 mask[dst_row:dst_row + rows] = True
-        if not np.array_equal(got[mask], llm[rank][mask]):
-            print(f"rank {rank} overlapped step {k}: llm rows differ", flush=True)
-            fails += 1
+        if proj is not None:
+            Ws, bs, d_enc = proj
+            ref = torch.zeros(len(mask), d_llm, device=dev)
+            for (i, src, dst_rank, dst_row, rows) in o["pieces"]:
+                if dst_rank != rank:
+                    continue
+                g = int(o["group"][i])
+                x = torch.from_numpy(odp.standin(int(t["ids"][i]), int(t["lens"][i]), d_enc[g])
+                                     .view(np.int16)).view(torch.bfloat16).to(dev)[:rows]
+                ref[dst_row:dst_row + rows] = x.float() @ Ws[g].to(dev).float().t() + \
+                    bs[g].to(dev).float()
+            m = torch.from_numpy(mask).to(dev)
+            err = (llm_got[k].float()[m] - ref[m]).abs()
+            if not bool((err <= 2.0 ** -7 * ref[m].abs() + 1e-3).all()):
+                print(f"rank {rank} overlapped step {k}: projected rows differ", flush=True)
+                fails += 1
+        else:
+            got = llm_got[k].cpu().view(torch.int16).numpy().view(np.uint16)
+            if not np.array_equal(got[mask], llm[rank][mask]):
+                print(f"rank {rank} overlapped step {k}: llm rows differ", flush=True)
+                fails += 1
         if rank == 0:
             print(f"overlapped step {k}: {int(o['recv_rows'].sum())} modality tokens ok="
                   f"{fails == 0}", flush=True)
@@ -130,13 +149,6 @@ def main():
                    lssp_eta=2048 if lssp else None, lssp_sp=world if lssp else 1,
                    reshard="cp_hybrid" if cp else "ulysses", cp_threshold=2048 if cp else 0,
                    overlap_dispatch=overlap)
-    if overlap:
-        path.method = "lpt_local"
-        fails = run_overlapped(path, name, cfg, world, rank, dev, gbs, dp, sp, d_in, d_llm)
-        t = torch.tensor([fails], device=dev)
-        dist.all_reduce(t)
-        dist.destroy_process_group()
-        sys.exit(1 if int(t.item()) else 0)
     if proj:
         gw = torch.Generator().manual_seed(9)
         Ws = [(torch.randn(d_llm, d_enc[g], generator=gw) / d_enc[g] ** 0.5).to(torch.bfloat16)
@@ -144,6 +156,14 @@ def main():
         bs = [torch.randn(d_llm, generator=gw).to(torch.bfloat16) for g in range(2)]
         for g in range(2):
             path.set_projector(g, Ws[g].to(dev), bs[g].to(dev))
+    if overlap:
+        path.method = "lpt_local"
+        fails = run_overlapped(path, name, cfg, world, rank, dev, gbs, dp, sp, d_in, d_llm,
+                               (Ws, bs, d_enc) if proj else None)
+        t = torch.tensor([fails], device=dev)
+        dist.all_reduce(t)
+        dist.destroy_process_group()
+        sys.exit(1 if int(t.item()) else 0)
     fails = 0
     for step in range(3):
         _, rest, drawn, chunks = owork.generate(descs, cfg["phases"], False, step, cfg["seed"],
