@@ -11,8 +11,13 @@ deterministic stand-in before timing.  Inputs are synthetic (the reference's
 own generator, restated in workload.py) and resident in HBM for `value`; `e2e`
 runs the same step through the public API from pinned host buffers.
 
+Steps are pipelined (MuxPath.run_pipeline): the plan of step k+1 runs on a
+side stream and, with the default --pipeline 2, its dispatch on a copy stream
+under step k's projector/return; the timed region covers K whole steps.
+
 Weak scaling: every GPU owns `gbs_per_replica` sequences (dp = N).
-Rank 0 prints one JSON line.
+Rank 0 prints one JSON line.  Tuning switches (env): MUX_GEMM_2CTA,
+MUX_CHUNK_BYTES, MUX_COPY_GRID, MUX_DISPATCH_GRID, MUX_COPY_GRAB.
 """
 
 from __future__ import annotations
