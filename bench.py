@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--reshard", default="ulysses", choices=["ulysses", "cp_hybrid"],
                     help="LLM placement over each replica's sp ranks")
     ap.add_argument("--cp-threshold", type=int, default=0, help="CpHybrid threshold (0: C/sp)")
+    ap.add_argument("--text-embed", action="store_true",
+                    help="also gather the text tokens' embedding rows into the packed LLM "
+                         "input every step (SURVEY §8f-4)")
     ap.add_argument("--graphs", type=int, default=0,
                     help="1: replay one captured CUDA graph per pipelined step")
     return ap.parse_args()
@@ -266,7 +269,8 @@ def run_ours(args):
                    group=group, method=args.method,
                    lssp_eta=args.lssp_eta if args.lssp_eta >= 0 else None,
                    lssp_sp=args.lssp_sp or world, reshard=args.reshard,
-                   cp_threshold=args.cp_threshold, overlap_dispatch=args.pipeline >= 2)
+                   cp_threshold=args.cp_threshold, overlap_dispatch=args.pipeline >= 2,
+                   text_embed=args.text_embed)
     if args.pipeline >= 2 and "MUX_DISPATCH_GRID" not in os.environ:
         path.dispatch_grid = -2 * path.num_sms  # lean copy CTAs beside the GEMM
     if projector:
@@ -296,6 +300,13 @@ def run_ours(args):
                                ret_bytes=int(h[_lib.H_RETURN_BYTES]),
                                disp_remote=int(h[_lib.H_DISPATCH_REMOTE]),
                                ret_remote=int(h[_lib.H_RETURN_REMOTE])))
+    text_tokens, text_table = [], None
+    if args.text_embed:  # synthetic token ids per distinct step, a 32K-row embedding table
+        text_table = torch.randn(32000, d_llm, device=dev).to(torch.bfloat16)
+        for t in tables:
+            n_text = int(sum(int(L) for L, m in zip(t.lens, t.mods) if m == 0))
+            text_tokens.append(torch.randint(0, 32000, (max(n_text, 1),), device=dev,
+                                             dtype=torch.int32))
     # encoder output: the stand-in fills it once (encoder compute is out of scope)
     plan = path.plan(dtabs[0])
     path.encode_standin(plan, dtabs[0])
@@ -327,9 +338,13 @@ def run_ours(args):
             for k in range(n):
                 one_step(k0 + k, timed_dom[k] if timed_dom else None)
             return
+        after = None
+        if args.text_embed:  # text rows of the packed LLM input, gathered after the return
+            def after(k, p, s):
+                path.embed_text(p, text_tokens[(k0 + k) % n_distinct], text_table, s)
         path.run_pipeline([(dtabs[(k0 + k) % n_distinct], arenas[(k0 + k) % n_distinct])
                            for k in range(n)], kernel_events=timed_dom, start_event=start_ev,
-                          stream=stream)
+                          stream=stream, after_step=after)
 
     graphs = None
     if args.graphs and args.pipeline:
@@ -452,6 +467,8 @@ def run_ours(args):
         launches += 1 + (1 if world > 1 else 0)
     if args.pipeline >= 2 and world > 1:
         launches += 2
+    if args.text_embed:
+        launches += 1
     line = {
         "metric": "multimodal tokens/s rebalanced+dispatched+scattered per step",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -470,6 +487,7 @@ def run_ours(args):
                    "lssp": ({"eta": args.lssp_eta, "group": args.lssp_sp or world}
                             if args.lssp_eta >= 0 else None),
                    "reshard": args.reshard if sp > 1 else None,
+                   "text_rows": bool(args.text_embed),
                    "launch": "one CUDA graph per step" if graphs is not None else "eager",
                    "llm_tokens_per_step": T_total / args.steps,
                    "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"},
