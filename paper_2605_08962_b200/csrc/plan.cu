@@ -236,7 +236,7 @@ Plan make_plan_const(const void* b, const mux_plan_layout& L) {
   return make_plan(const_cast<void*>(b), L);
 }
 
-// Phase timestamps (globaltimer, ns) in header slots 16..31 for profiling.
+// Phase timestamps (globaltimer, ns): stamp slot 16..25 -> header slot 20..29.
 __device__ __forceinline__ void stamp(Plan& p, int slot) {
   if (threadIdx.x == 0) {
     uint64_t t;

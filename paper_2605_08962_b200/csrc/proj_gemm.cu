@@ -8,13 +8,15 @@
 // adapter sits between the encoder and the LLM and this
 // fuses it with the return scatter.
 //
-// Persistent, one CTA per SM, warp-specialised:
-//   warp 0      TMA producer: A tile 128x64 and B tile 256x64 per stage
-//               (128-byte swizzle), 4-stage mbarrier ring
-//   warp 1      TMEM owner + single-thread tcgen05.mma issuer (M128 N256 K16)
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> +bias -> bf16 -> row store
-// Two 256-column fp32 accumulators in TMEM (all 512 columns) let the
-// epilogue of tile i overlap the MMAs of tile i+1.
+// Two kernels, both persistent and warp-specialised (warp 0 TMA producer,
+// warp 1 TMEM owner + single-thread MMA issuer, 8 epilogue warps draining
+// two 256-column fp32 TMEM accumulators so the epilogue of tile i overlaps the
+// MMAs of tile i+1; tcgen05.ld 32x32b.x32 -> +bias -> bf16 -> row stores):
+//   proj_scatter_kernel       one CTA per SM, M128 N256 K16, 4-stage ring of
+//                             A 128x64 + B 256x64 (128-byte swizzle)
+//   proj_scatter_pair_kernel  (default) CTA pairs, tcgen05.mma.cta_group::2
+//                             M256 N256 K16, 6-stage ring of half tiles (below)
+// Both handle up to two problems (encoder groups) per launch.
 
 #include <cuda.h>
 #include <cuda_bf16.h>

@@ -129,8 +129,9 @@ struct SegArgs {
   int32_t grab;         // chunks per grab (0: adaptive)
 };
 
-// Work distribution is dynamic: CTAs grab kGrab chunks at a time from a
-// device counter (the next grab is fetched while the current one copies), so
+// Work distribution is dynamic: CTAs grab chunks (1 for a local copy, kGrab
+// for a cross-GPU exchange) from a device counter (the next grab is fetched
+// while the current one copies), so
 // CTAs that start late — e.g. next to the side-stream planner — take less.
 // Each grab locates its first segment by binary search over the chunk prefix
 // (staged in shared memory when it fits) and walks forward.
