@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int g, m_blk, n_blk;
         locate(tm, G, num_n, tile, g, m_blk, n_blk);
         for (int kb = 0; kb < tm.kblocks[g]; ++kb) {
-          mbar_wait_bounded(&empty[stage], phase ^ 1, true);
+          mbar_wait_bounded(&empty[stage], phase ^ 1, false);
           uint8_t* sa = smem + stage * STAGE2_BYTES;
           if (leader) mbar_expect_tx(&full[stage], 2 * STAGE2_BYTES);
           const uint32_t bar = smem_u32(&full[stage]) & kPeerBitMask;
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
         int g, m_blk, n_blk;
         locate(tm, G, num_n, tile, g, m_blk, n_blk);
-        mbar_wait_bounded(&tempty[acc], acc_phase ^ 1, true);
+        mbar_wait_bounded(&tempty[acc], acc_phase ^ 1, false);
         fence_after();
         const uint32_t d = tmem_base + acc * BN;
         for (int kb = 0; kb < tm.kblocks[g]; ++kb) {
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         my_dst = static_cast<char*>(P.out_bases[rd >> 40]) +
                  ((rd & kRowMask) * N + (int64_t)n_blk * BN + colgrp * 128) * 2;
       }
-      mbar_wait_bounded(&tfull[acc], acc_phase, true);
+      mbar_wait_bounded(&tfull[acc], acc_phase, false);
       fence_after();
 #pragma unroll 1
       for (int sub = 0; sub < 2; ++sub) {

@@ -200,9 +200,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
+// Arrive on an mbarrier of another CTA of the cluster (default semantics, as
+// CUTLASS's ClusterBarrier::arrive).  The pair GEMM's epilogue only needs its
+// TMEM reads ordered before the leader's next MMA, which tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync provide; a release.cluster arrive made
+// every epilogue warp wait for its global stores (MEMBAR + ERRBAR per tile).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load into this CTA's smem, completing bytes on an mbarrier of either
 // CTA of the pair (the leader's, addressed with the peer bit cleared).
