@@ -24,7 +24,7 @@ def test_push_exchange_bit_exact(config):
     n = _ngpus()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    world = min(n, 8)
+    world = min(n, 4)  # 2-4 ranks cover the protocol; keeps the oracle's host work bounded
     if config.startswith("cfg4") and world % 4:
         world = 2  # dp=2 x sp=1 fallback when sp=4 does not divide
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
