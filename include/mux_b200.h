@@ -259,6 +259,11 @@ int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t
                void* stream);
 int mux_wait(int32_t world, const uint64_t* my_flags, const uint64_t* epoch_ctr,
              int32_t timeout_ms, int32_t* err_dev, void* stream);
+/* mux_signal with fence = 0: no system-scope fence before the flag stores.
+ * For a permission signal ("my buffer may be overwritten") issued after
+ * kernels that only read that buffer: stream order already completed them. */
+int mux_signal_ex(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t* epoch_ctr,
+                  int32_t fence, void* stream);
 
 /* Deterministic encoder stand-in: for every sample of rank `me` in group
  * `group`, rows [enc_off, enc_off+len) of out (row width `width` bf16)

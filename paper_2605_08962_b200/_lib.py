@@ -83,6 +83,7 @@ _SIGS = [
     ("mux_memcpy_async", C.c_int, [_P, _P, C.c_int64, _P]),
     ("mux_signal", C.c_int, [C.c_int32, C.c_int32, _P, _P, _P]),
     ("mux_wait", C.c_int, [C.c_int32, _P, _P, C.c_int32, _P, _P]),
+    ("mux_signal_ex", C.c_int, [C.c_int32, C.c_int32, _P, _P, C.c_int32, _P]),
     ("mux_encoder_standin", C.c_int, [C.POINTER(PlanCfg), _P, _P, _P, C.c_int32, C.c_int32, _P,
                                       _P]),
     ("mux_return_rows", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, C.c_int64, _P]),

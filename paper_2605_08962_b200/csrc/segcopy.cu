@@ -215,15 +215,20 @@ __global__ void __launch_bounds__(kCopyThreads) copy_bytes_kernel(char* dst, con
 }
 
 __global__ void signal_kernel(int me, int world, uint64_t* const* flags_peers,
-                              uint64_t* epoch_ctr) {
+                              uint64_t* epoch_ctr, int fence) {
   const int r = threadIdx.x;
   const uint64_t e = *epoch_ctr + 1;
   __syncwarp();
   if (r == 0) *epoch_ctr = e;
-  __threadfence_system();
+  // fence = 0: a pure permission ("my buffer may be overwritten") after
+  // kernels that only READ it; stream order already completed those reads
+  if (fence) __threadfence_system();
   if (r < world) {
     uint64_t* f = flags_peers[r] + me;
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+    if (fence)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+    else
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
   }
 }
 
@@ -464,8 +469,13 @@ extern "C" int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t
 
 extern "C" int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers,
                           uint64_t* epoch_ctr, void* stream) {
+  return mux_signal_ex(me, world, flags_peers, epoch_ctr, 1, stream);
+}
+
+extern "C" int mux_signal_ex(int32_t me, int32_t world, uint64_t* const* flags_peers,
+                             uint64_t* epoch_ctr, int32_t fence, void* stream) {
   signal_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(me, world, flags_peers,
-                                                                 epoch_ctr);
+                                                                 epoch_ctr, fence);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

@@ -365,10 +365,11 @@ class MuxPath:
     def signal_consumed(self, stream=None):
         """This rank's encoder has read its receive windows (E channel): peers may
         push the next step's rows (dispatch_overlapped)."""
-        if self.world > 1:
-            _lib.check(_lib.lib().mux_signal(self.rank, self.world, self.flag_ptrs_e.data_ptr(),
-                                             self.epoch_e.data_ptr(), _stream_ptr(stream)),
-                       "mux_signal")
+        if self.world > 1:  # a permission, not data: no system fence (mux_signal_ex)
+            _lib.check(_lib.lib().mux_signal_ex(self.rank, self.world,
+                                                self.flag_ptrs_e.data_ptr(),
+                                                self.epoch_e.data_ptr(), 0,
+                                                _stream_ptr(stream)), "mux_signal_ex")
 
     def dispatch_overlapped(self, plan: Plan, arenas, stream, after=None):
         """The next step's dispatch on its own `stream`, under the current step's
