@@ -465,8 +465,8 @@ def run_ours(args):
         launches += 2 + (1 if world > 1 else 0)
     else:
         launches += 1 + (1 if world > 1 else 0)
-    if args.pipeline >= 2 and world > 1:
-        launches += 2
+    if args.pipeline >= 2 and world > 1:  # consumed wait (+ its signal unless fused in the GEMM)
+        launches += 1 if (projector and not path.staged) else 2
     if args.text_embed:
         launches += 1
     line = {

@@ -259,6 +259,11 @@ int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t
                void* stream);
 int mux_wait(int32_t world, const uint64_t* my_flags, const uint64_t* epoch_ctr,
              int32_t timeout_ms, int32_t* err_dev, void* stream);
+/* mux_wait for an explicit epoch (known to the host) instead of the value of
+ * this rank's own counter — for a wait issued on a stream that does not
+ * follow the signalling launch. */
+int mux_wait_value(int32_t world, const uint64_t* my_flags, uint64_t target, int32_t timeout_ms,
+                   int32_t* err_dev, void* stream);
 /* mux_signal with fence = 0: no system-scope fence before the flag stores.
  * For a permission signal ("my buffer may be overwritten") issued after
  * kernels that only read that buffer: stream order already completed them. */
@@ -333,11 +338,15 @@ int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_groups, int
 /* Same, and the launch's last CTA then publishes the next epoch to every
  * peer (mux_signal fused into the GEMM: every row store, local or NVLink,
  * is fenced at system scope before the flag).  sync: a zeroed uint32 the
- * kernel re-arms. */
+ * kernel re-arms.  e_flags_peers / e_epoch_ctr (optional, NULL = none): a
+ * second channel signalled at kernel START without a fence — the
+ * "receive windows consumed" permission (mux_signal_ex with fence 0) fused
+ * into the launch. */
 int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int32_t n_groups, int32_t N,
                                     void* const* out_bases, int32_t num_sms, int32_t me,
                                     int32_t world, uint64_t* const* flags_peers, uint32_t* sync,
-                                    uint64_t* epoch_ctr, void* stream);
+                                    uint64_t* epoch_ctr, uint64_t* const* e_flags_peers,
+                                    uint64_t* e_epoch_ctr, void* stream);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,7 @@ _SIGS = [
     ("mux_signal", C.c_int, [C.c_int32, C.c_int32, _P, _P, _P]),
     ("mux_wait", C.c_int, [C.c_int32, _P, _P, C.c_int32, _P, _P]),
     ("mux_signal_ex", C.c_int, [C.c_int32, C.c_int32, _P, _P, C.c_int32, _P]),
+    ("mux_wait_value", C.c_int, [C.c_int32, _P, C.c_uint64, C.c_int32, _P, _P]),
     ("mux_encoder_standin", C.c_int, [C.POINTER(PlanCfg), _P, _P, _P, C.c_int32, C.c_int32, _P,
                                       _P]),
     ("mux_return_rows", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, C.c_int64, _P]),
@@ -98,7 +99,7 @@ _SIGS = [
                                            C.c_int32, _P]),
     ("mux_proj_scatter_grouped_signal", C.c_int, [C.POINTER(ProjGroup), C.c_int32, C.c_int32,
                                                   _P, C.c_int32, C.c_int32, C.c_int32, _P, _P,
-                                                  _P, _P]),
+                                                  _P, _P, _P, _P]),
 ]
 EXPORTS = tuple(n for n, _, _ in _SIGS)
 

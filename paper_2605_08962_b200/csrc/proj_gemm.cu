@@ -66,7 +66,22 @@ struct GroupParams {
   uint64_t* epoch_ctr;
   uint32_t* ticket;  // zero before the first launch; re-armed by the last CTA
   int me, world;
+  // optional "consumed" signal at kernel start (E channel, relaxed stores; the
+  // kernels before this one in the stream only read the receive windows)
+  uint64_t* const* e_flags_peers;
+  uint64_t* e_epoch_ctr;
 };
+
+// E signal by one thread at kernel start (see GroupParams).
+__device__ __forceinline__ void consumed_signal(const GroupParams& P) {
+  if (!P.e_flags_peers) return;
+  const uint64_t e = *P.e_epoch_ctr + 1;
+  *P.e_epoch_ctr = e;
+  for (int r = 0; r < P.world; ++r) {
+    uint64_t* f = P.e_flags_peers[r] + P.me;
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+  }
+}
 
 struct TileMap {
   int64_t tiles[kMaxGroups + 1];  // first tile of each group, then the total
@@ -137,6 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t num_tiles = tm.tiles[G];
 
   if (warp == 0 && lane == 0) {
+    if (blockIdx.x == 0) consumed_signal(P);
     for (int g = 0; g < G; ++g) {
       tma_prefetch(&P.ta[g]);
       tma_prefetch(&P.tb[g]);
@@ -359,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t num_tiles = tm.tiles[G];
 
   if (warp == 0 && lane == 0) {
+    if (blockIdx.x == 0) consumed_signal(P);
     for (int g = 0; g < G; ++g) {
       tma_prefetch(&P.ta[g]);
       tma_prefetch(&P.tb[g]);
@@ -588,14 +605,16 @@ extern "C" int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_
                                         int32_t N, void* const* out_bases, int32_t num_sms,
                                         void* stream) {
   return mux_proj_scatter_grouped_signal(groups, n_groups, N, out_bases, num_sms, 0, 0, nullptr,
-                                         nullptr, nullptr, stream);
+                                         nullptr, nullptr, nullptr, nullptr, stream);
 }
 
 extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int32_t n_groups,
                                                int32_t N, void* const* out_bases, int32_t num_sms,
                                                int32_t me, int32_t world,
                                                uint64_t* const* flags_peers, uint32_t* sync,
-                                               uint64_t* epoch_ctr, void* stream) {
+                                               uint64_t* epoch_ctr,
+                                               uint64_t* const* e_flags_peers,
+                                               uint64_t* e_epoch_ctr, void* stream) {
   using namespace proj;
   if (world > 0 && (!flags_peers || !sync || !epoch_ctr || world > 32 || me < 0 || me >= world)) {
     set_error("projector signal: need flags, sync and epoch pointers, 0 <= me < world <= 32");
@@ -638,8 +657,14 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
   P.ticket = sync;
   P.me = me;
   P.world = world;
+  P.e_flags_peers = world > 0 ? e_flags_peers : nullptr;
+  P.e_epoch_ctr = e_epoch_ctr;
   if (P.n_groups == 0) {
-    // nothing to compute: still publish the epoch (peers wait for it)
+    // nothing to compute: still publish the epochs (peers wait for them)
+    if (P.e_flags_peers) {
+      int st = mux_signal_ex(me, world, e_flags_peers, e_epoch_ctr, 0, stream);
+      if (st) return st;
+    }
     return world > 0 ? mux_signal(me, world, flags_peers, epoch_ctr, stream) : MUX_OK;
   }
   static int pair = -1;  // the CTA-pair (cta_group::2) kernel unless MUX_GEMM_2CTA=0

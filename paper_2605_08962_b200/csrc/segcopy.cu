@@ -239,10 +239,10 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 
 __global__ void wait_kernel(int world, const uint64_t* flags, const uint64_t* epoch_ctr,
-                            int64_t timeout_ns, int32_t* err) {
+                            uint64_t target, int64_t timeout_ns, int32_t* err) {
   const int r = threadIdx.x;
   if (r >= world) return;
-  const uint64_t epoch = *epoch_ctr;
+  const uint64_t epoch = epoch_ctr ? *epoch_ctr : target;
   const uint64_t t0 = global_ns();
   for (;;) {
     uint64_t v;
@@ -482,7 +482,16 @@ extern "C" int mux_signal_ex(int32_t me, int32_t world, uint64_t* const* flags_p
 
 extern "C" int mux_wait(int32_t world, const uint64_t* my_flags, const uint64_t* epoch_ctr,
                         int32_t timeout_ms, int32_t* err_dev, void* stream) {
-  wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(world, my_flags, epoch_ctr,
+  wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(world, my_flags, epoch_ctr, 0,
+                                                               (int64_t)timeout_ms * 1000000,
+                                                               err_dev);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_wait_value(int32_t world, const uint64_t* my_flags, uint64_t target,
+                              int32_t timeout_ms, int32_t* err_dev, void* stream) {
+  wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(world, my_flags, nullptr, target,
                                                                (int64_t)timeout_ms * 1000000,
                                                                err_dev);
   MUX_CUDA(cudaGetLastError());

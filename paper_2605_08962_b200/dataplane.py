@@ -138,6 +138,8 @@ class MuxPath:
         self.flags_e.tensor.zero_()
         self.epoch_d = torch.zeros(1, dtype=torch.int64, device=dev)
         self.epoch_e = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._e_sent = 0  # E signals issued (host count = the device epoch_e)
+        self._fuse_e = False  # the next fused projector launch carries the E signal
         self.enc_out = [torch.empty(rows * self.d_ret[g], dtype=torch.bfloat16, device=dev)
                         for g in range(N_GROUPS)]
         # copy counters x3 tables, then the projector's completion ticket
@@ -302,17 +304,19 @@ class MuxPath:
             if encoder is not None:
                 encoder(k, p, main)
             if ov:
-                self.signal_consumed(main)
-                if k + 1 < n:
-                    ev = _event()
-                    ev.record(main)
-                    cs.wait_event(self._ready[slot[k + 1]])
-                    self.dispatch_overlapped(self._ring[slot[k + 1]], steps[k + 1][1], cs,
-                                             after=ev)
-                    self._dispatched[slot[k + 1]].record(cs)
+                self.signal_consumed(main, fuse=True)
+                ev = _event()
+                ev.record(main)
             self.kernel_events = kernel_events[k] if kernel_events else None
             self._freed[s] = self.return_scatter(p, main)
             self.kernel_events = None
+            if ov and k + 1 < n:
+                # issued after the return kernel: the copy stream's spin-wait for
+                # every rank's "consumed" signal (carried by that kernel) must never
+                # sit in front of it in a shared hardware queue
+                cs.wait_event(self._ready[slot[k + 1]])
+                self.dispatch_overlapped(self._ring[slot[k + 1]], steps[k + 1][1], cs, after=ev)
+                self._dispatched[slot[k + 1]].record(cs)
             if after_step is not None:
                 after_step(k, p, main)
         self._kstep = base + n
@@ -362,14 +366,22 @@ class MuxPath:
         """Pack + dispatch: loader rows of every group to their encoder rank."""
         self._exchange(plan, 0, self._arena_table(arenas), self.recv_dst, stream)
 
-    def signal_consumed(self, stream=None):
+    def signal_consumed(self, stream=None, fuse: bool = False):
         """This rank's encoder has read its receive windows (E channel): peers may
-        push the next step's rows (dispatch_overlapped)."""
-        if self.world > 1:  # a permission, not data: no system fence (mux_signal_ex)
-            _lib.check(_lib.lib().mux_signal_ex(self.rank, self.world,
-                                                self.flag_ptrs_e.data_ptr(),
-                                                self.epoch_e.data_ptr(), 0,
-                                                _stream_ptr(stream)), "mux_signal_ex")
+        push the next step's rows (dispatch_overlapped).  fuse=True: the next
+        return_scatter's projector GEMM carries the signal at its start instead
+        of a separate launch."""
+        if self.world == 1:
+            return
+        self._e_sent += 1
+        if fuse and self.projector and not self.staged and \
+                os.environ.get("MUX_FUSE_E", "1") != "0":
+            self._fuse_e = True
+            return
+        # a permission, not data: no system fence (mux_signal_ex)
+        _lib.check(_lib.lib().mux_signal_ex(self.rank, self.world, self.flag_ptrs_e.data_ptr(),
+                                            self.epoch_e.data_ptr(), 0, _stream_ptr(stream)),
+                   "mux_signal_ex")
 
     def dispatch_overlapped(self, plan: Plan, arenas, stream, after=None):
         """The next step's dispatch on its own `stream`, under the current step's
@@ -380,11 +392,11 @@ class MuxPath:
             raise ValueError("MuxPath(overlap_dispatch=True) is needed")
         if after is not None:
             stream.wait_event(after)
-        if self.world > 1:
-            _lib.check(_lib.lib().mux_wait(self.world, self.flags_e.tensor.data_ptr(),
-                                           self.epoch_e.data_ptr(), self.timeout_ms,
-                                           self.wait_err.data_ptr(), _stream_ptr(stream)),
-                       "mux_wait")
+        if self.world > 1:  # every peer's E count reaches mine (host-known target)
+            _lib.check(_lib.lib().mux_wait_value(self.world, self.flags_e.tensor.data_ptr(),
+                                                 self._e_sent, self.timeout_ms,
+                                                 self.wait_err.data_ptr(), _stream_ptr(stream)),
+                       "mux_wait_value")
         self.dispatch(plan, arenas, stream)
 
     def encode_standin(self, plan: Plan, dtab: DeviceTable, stream=None):
@@ -453,12 +465,15 @@ class MuxPath:
                                                   self.llm_dst[self.last_llm].data_ptr(),
                                                   self.gemm_ctas, s),
                        "mux_proj_scatter_grouped")
-        else:  # the GEMM's last CTA signals every peer
+        else:  # the GEMM's last CTA signals every peer (+ a pending E signal at its start)
+            fe = self._fuse_e
+            self._fuse_e = False
             _lib.check(L.mux_proj_scatter_grouped_signal(
                 groups, n, self.d_llm, self.llm_dst[self.last_llm].data_ptr(), self.gemm_ctas,
                 self.rank,
                 self.world, self.flag_ptrs.data_ptr(), self.sync[6:].data_ptr(),
-                self.epoch_ctr.data_ptr(), s), "mux_proj_scatter_grouped_signal")
+                self.epoch_ctr.data_ptr(), self.flag_ptrs_e.data_ptr() if fe else None,
+                self.epoch_e.data_ptr() if fe else None, s), "mux_proj_scatter_grouped_signal")
         if ke is not None:
             ke[1].record(main)
         if self.world > 1:
