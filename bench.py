@@ -17,7 +17,8 @@ under step k's projector/return; the timed region covers K whole steps.
 
 Weak scaling: every GPU owns `gbs_per_replica` sequences (dp = N).
 Rank 0 prints one JSON line.  Tuning switches (env): MUX_GEMM_2CTA,
-MUX_CHUNK_BYTES, MUX_COPY_GRID, MUX_DISPATCH_GRID, MUX_COPY_GRAB.
+MUX_CHUNK_BYTES, MUX_COPY_GRID, MUX_DISPATCH_GRID, MUX_COPY_GRAB, MUX_FUSE_E,
+MUX_PROJECTOR_RETURN.
 """
 
 from __future__ import annotations
