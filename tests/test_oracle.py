@@ -331,3 +331,21 @@ def test_cphybrid_matches_plan_reshard_on_golden_steps():
                 assert sum(int(x.sum()) for x in cover) + text == int(c["llm_rows"].sum())
                 n += 1
     assert n >= 12
+
+
+def test_cphybrid_threshold_monotone():
+    """SPEC.md reshard invariant: raising cp_threshold never increases the number of
+    sharded samples; loads are conserved per sequence."""
+    for name, st, t, _ in golden_steps():
+        if st["world"] != 1 or st["step"] > 0:
+            continue
+        o = oplan.plan_step(t, configs.CAPACITY, st["gbs"], 1, 4, 4)
+        prev = None
+        for thr in (64, 512, 2048, 4096, 16384):
+            c = ocph.place(o, t, st["gbs"], 1, 4, configs.CAPACITY, thr)
+            lens = np.asarray(t["lens"])
+            sharded = sum(1 for i in range(len(lens))
+                          if 0 <= o["seq"][i] < st["gbs"] and lens[i] > thr)
+            assert prev is None or sharded <= prev
+            prev = sharded
+            assert c["shard_len"].sum(axis=1).tolist() == o["fills"][:st["gbs"]].tolist()
