@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--pipeline", type=int, default=2,
                     help="1: plan step k+1 on a side stream during step k; 2 (default): also "
                          "dispatch step k+1 under step k's return")
-    ap.add_argument("--method", default="lpt_local", choices=["lpt", "kk", "lpt_local"],
+    ap.add_argument("--method", default="lpt_local",
+                    choices=["lpt", "kk", "lpt_local", "lpt_local_rw"],
                     help="encoder balancing: locality-first LPT (default), LPT or KK")
     ap.add_argument("--hang-dump", type=float, default=0.0,
                     help="dump Python stacks after this many seconds (debug)")

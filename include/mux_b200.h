@@ -60,6 +60,8 @@ extern "C" {
 #define MUX_KK 1
 #define MUX_LPT_LOCAL 2 /* locality-first LPT: keep samples on their origin rank up to
                            the balanced load, LPT the rest on top */
+#define MUX_LPT_LOCAL_RW 3 /* as MUX_LPT_LOCAL, but pass 2 charges a sample 9/8 of its
+                              cost on a rank other than its origin (NVLink-moved rows) */
 
 #define MUX_N_GROUPS 2 /* encoder groups: 0 = vision (image/video), 1 = audio */
 

@@ -49,7 +49,7 @@ def lpt_assign(costs, ids, g, init=None):
     return out
 
 
-def lpt_local_assign(costs, ids, origins, g):
+def lpt_local_assign(costs, ids, origins, g, remote_weight=False):
     """Locality-first LPT (builder's variant of the north_star's greedy/LPT; the
     reference balances with KK over the whole group, moving
     almost every sample).  In LPT order (-cost, id, index): pass 1 keeps an item
@@ -72,9 +72,13 @@ def lpt_local_assign(costs, ids, origins, g):
             pool.append(i)
     load = list(kept)
     for i in pool:
-        r = min(range(g), key=lambda k: (load[k], k))
+        # remote_weight: 9/8 of the cost on a rank other than the origin (exact:
+        # integer costs, multiples of 1/8); the smallest resulting load wins
+        ce = [costs[i] * 1.125 if remote_weight and k != origins[i] else costs[i]
+              for k in range(g)]
+        r = min(range(g), key=lambda k: (load[k] + ce[k], k))
         out[i] = r
-        load[r] = load[r] + costs[i]
+        load[r] = load[r] + ce[r]
     return out
 
 
@@ -249,9 +253,10 @@ def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=F
             ranks = lpt_assign(costs, [int(ids[i]) for i in items], world)
         elif method == "kk":
             ranks = kk_assign(costs, world)
-        elif method == "lpt_local":
+        elif method in ("lpt_local", "lpt_local_rw"):
             ranks = lpt_local_assign(costs, [int(ids[i]) for i in items],
-                                     [int(origin[i]) for i in items], world)
+                                     [int(origin[i]) for i in items], world,
+                                     remote_weight=method == "lpt_local_rw")
         else:
             raise ValueError(f"unknown method {method!r}")
         for i, r in zip(items, ranks):

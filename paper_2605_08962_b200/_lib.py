@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmuxb200.
 
 MUX_OK, MUX_ERR_CONFIG, MUX_ERR_PACKING, MUX_ERR_VALUE, MUX_ERR_CUDA, MUX_ERR_RUNTIME = range(6)
 MODE_PACK, MODE_STEP = 0, 1
-LPT, KK, LPT_LOCAL = 0, 1, 2
+LPT, KK, LPT_LOCAL, LPT_LOCAL_RW = 0, 1, 2, 3
 N_GROUPS = 2
 
 H_STATUS, H_ERR_INDEX, H_N_SEQ, H_N_DISPATCH, H_N_RETURN = 0, 1, 2, 3, 4

@@ -315,7 +315,7 @@ __device__ void lpt_warp(const int* s_ord, const double* cost, int n, int g, int
 // integer-valued costs every sum is exact, so it matches the CPU oracle bit
 // for bit (oracle/planner.py:lpt_local_assign).
 __device__ void lpt_local_warp(const int* s_ord, const double* cost, const int32_t* origin, int n,
-                               int g, int32_t* out_rank, int32_t* s_kept_flag) {
+                               int g, int32_t* out_rank, int32_t* s_kept_flag, bool remote_w) {
   const int lane = threadIdx.x & 31;
   double part = 0.0;
   for (int q = lane; q < n; q += 32) part += cost[s_ord[q]];
@@ -341,7 +341,11 @@ __device__ void lpt_local_warp(const int* s_ord, const double* cost, const int32
     if (s_kept_flag[q]) continue;
     const int k = s_ord[q];
     const double c = cost[k];
-    double l = lane < g ? load : __longlong_as_double(0x7ff0000000000000LL);
+    // remote_w: the item costs 9/8 c on a rank other than its origin; the rank
+    // with the smallest resulting load wins (lowest rank on ties).  Costs are
+    // integers, so every value is a multiple of 1/8 and exact.
+    const double ce = remote_w && lane != origin[k] ? __dmul_rn(c, 1.125) : c;
+    double l = lane < g ? __dadd_rn(load, ce) : __longlong_as_double(0x7ff0000000000000LL);
     int r = lane;
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) {
@@ -353,7 +357,7 @@ __device__ void lpt_local_warp(const int* s_ord, const double* cost, const int32
       }
     }
     r = __shfl_sync(MUX_FULL, r, 0);
-    if (lane == r) load = __dadd_rn(load, c);
+    if (lane == r) load = __dadd_rn(load, ce);
     if (lane == 0) out_rank[k] = r;
   }
   __syncwarp();
@@ -991,16 +995,18 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
   if (m > 0) {
     if (W == 1) {
       for (int v = tid; v < m; v += nt) l_rank[v] = 0;
-    } else if (cfg.method == MUX_LPT || cfg.method == MUX_LPT_LOCAL) {
+    } else if (cfg.method == MUX_LPT || cfg.method == MUX_LPT_LOCAL ||
+               cfg.method == MUX_LPT_LOCAL_RW) {
       bitonic_sort(l_ord, next_pow2(m), PoolKey{l_pool, l_cost, l_id, l_tidx, m});
       const int warp = tid >> 5;
       if (cfg.method == MUX_LPT) {
         if (warp == 0 && m0 > 0) lpt_warp(l_ord, l_cost, m0, W, l_rank);
         if (warp == 1 && m1 > 0) lpt_warp(l_ord + m0, l_cost, m1, W, l_rank);
       } else {
-        if (warp == 0 && m0 > 0) lpt_local_warp(l_ord, l_cost, l_org, m0, W, l_rank, l_flag);
+        const bool rw = cfg.method == MUX_LPT_LOCAL_RW;
+        if (warp == 0 && m0 > 0) lpt_local_warp(l_ord, l_cost, l_org, m0, W, l_rank, l_flag, rw);
         if (warp == 1 && m1 > 0)
-          lpt_local_warp(l_ord + m0, l_cost, l_org, m1, W, l_rank, l_flag + m0);
+          lpt_local_warp(l_ord + m0, l_cost, l_org, m1, W, l_rank, l_flag + m0, rw);
       }
     } else if (m0 > kKkMax || m1 > kKkMax) {
       if (tid == 0) p.hdr[MUX_H_ERR_INDEX] = -2;  // KK pool limit

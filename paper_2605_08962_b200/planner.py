@@ -23,7 +23,8 @@ from ._lib import PlanCfg, PlanLayout
 from .configs import GROUP_OF_MOD
 from .workload import MODALITY_CODE, PackedSequence, Sample
 
-METHODS = {"lpt": _lib.LPT, "kk": _lib.KK, "lpt_local": _lib.LPT_LOCAL}
+METHODS = {"lpt": _lib.LPT, "kk": _lib.KK, "lpt_local": _lib.LPT_LOCAL,
+           "lpt_local_rw": _lib.LPT_LOCAL_RW}
 DEFAULT_CHUNK_BYTES = 32768
 
 

@@ -48,7 +48,7 @@ def assert_plan_equal(d, o, t, me):
     assert np.array_equal(d["gseg"], odp.grad_by_rank(o, me))
 
 
-@pytest.mark.parametrize("method", ["lpt", "kk", "lpt_local"])
+@pytest.mark.parametrize("method", ["lpt", "kk", "lpt_local", "lpt_local_rw"])
 def test_plan_matches_oracle_on_golden_steps(cuda_device, method):
     n = 0
     for name, st, t, _ in golden_steps():
@@ -69,7 +69,7 @@ def test_plan_matches_oracle_random_tables(cuda_device):
         world, dp = [(1, 1), (2, 2), (2, 1), (4, 4), (4, 2), (8, 8), (8, 2), (8, 1)][it % 8]
         sp = world // dp
         gbs = dp * int(rs.randint(1, 3))
-        method = ("kk", "lpt", "lpt_local")[it % 3]
+        method = ("kk", "lpt", "lpt_local", "lpt_local_rw")[it % 4]
         pooled = it % 5 == 0
         try:
             o = oplan.plan_step(t, cap, gbs, dp, sp, world, 1, method, pooled)
