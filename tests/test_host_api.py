@@ -129,3 +129,29 @@ def test_ctypes_struct_mirrors_match_the_library():
     _lib.lib().mux_abi_sizes(out)
     assert list(out) == [C.sizeof(_lib.PlanCfg), C.sizeof(_lib.PlanLayout),
                          C.sizeof(_lib.ProjGroup)]
+
+
+def test_header_is_plain_c99(tmp_path):
+    """include/mux_b200.h is a C ABI: it compiles as strict C99 (no C++ or CUDA types)
+    and a C program linking libmuxb200.so sees the same struct sizes as ctypes."""
+    import ctypes as C
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "t.c"
+    src.write_text(
+        '#include <stdio.h>\n#include "mux_b200.h"\n'
+        "int main(void) { printf(\"%zu %zu %zu\\n\", sizeof(mux_plan_cfg),"
+        " sizeof(mux_plan_layout), sizeof(mux_proj_group)); return mux_version() > 0 ? 0 : 1; }\n")
+    exe = tmp_path / "t"
+    libdir = os.path.join(ROOT, "paper_2605_08962_b200")
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror",
+                        "-I", os.path.join(ROOT, "include"), str(src), "-L", libdir,
+                        "-lmuxb200", "-Wl,-rpath," + libdir, "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert [int(x) for x in out.stdout.split()] == [
+        C.sizeof(_lib.PlanCfg), C.sizeof(_lib.PlanLayout), C.sizeof(_lib.ProjGroup)]
