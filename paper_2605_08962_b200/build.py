@@ -50,7 +50,8 @@ def _compile(src):
     obj = os.path.join(OBJ, src.replace(".cu", ".o"))
     srcp = os.path.join(CSRC, src)
     if _stale(obj, [srcp] + _deps()):
-        cmd = [NVCC, *FLAGS, "-c", srcp, "-o", obj]
+        cmd = [NVCC, *FLAGS, *os.environ.get("MUX_NVCC_DEFS", "").split(), "-c", srcp,
+               "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
