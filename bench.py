@@ -515,9 +515,10 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
 
     Every step copies its step table and loader payload host->device and reads
     its plan header back (D2H), inside the timed region.  Like a data loader
-    with pinned memory, the upload of step k+1 runs on a copy stream and the
-    plan of step k+1 on the planner stream while step k's rows move; two
-    device input slots alternate."""
+    with pinned memory, the upload of step k+1 runs on a copy stream
+    (MuxPath.run_pipeline's `prepare`) and its plan on the planner stream while
+    step k's rows move, with the same overlapped dispatch as `value`; two device
+    input slots alternate."""
     import torch
     import torch.distributed as dist
 
@@ -537,12 +538,12 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
     uploaded = [torch.cuda.Event() for _ in range(2)]
     consumed = [None, None]
     steps = max(args.steps, 3)
-    R = path.RING
-    dtabs = [None, None]
+    counts = {"h2d": 0, "d2h": 0}
 
-    def upload(k):
+    def prepare(k):
+        """Upload step k into input slot k % 2 (the loader side of the pipeline)."""
         i, slot = k % n_distinct, k % 2
-        if consumed[slot] is not None:
+        if consumed[slot] is not None:  # step k-2 is done with this slot
             up.wait_event(consumed[slot])
         with torch.cuda.stream(up):
             blob = dev_tab[slot][: host_tabs[i].numel()]
@@ -551,51 +552,32 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
                 n = host_ar[i][g].numel()
                 dev_ar[slot][g][:n].copy_(host_ar[i][g].view(-1), non_blocking=True)
         uploaded[slot].record(up)
-        dt = DeviceTable.__new__(DeviceTable)  # view of the uploaded blob
-        dt.table, dt.blob = tables[i], blob
-        S, nc = tables[i].S, tables[i].n_carry
-        base = blob.data_ptr()
-        dt.ids, dt.lens, dt.mods = base, base + 8 * S, base + 12 * S
-        dt.carry_seq, dt.chunk_off = base + 16 * S, base + 16 * S + 4 * nc
-        dtabs[slot] = dt
-        path.plan_ahead(dt, k % R, after=uploaded[slot])
-        return host_tabs[i].numel() * 8 + sum(b.numel() * 2 for b in host_ar[i])
+        counts["h2d"] += host_tabs[i].numel() * 8 + sum(b.numel() * 2 for b in host_ar[i])
+        shaped = [dev_ar[slot][g][: host_ar[i][g].numel()].view(host_ar[i][g].shape)
+                  for g in range(2)]
+        return DeviceTable.from_blob(tables[i], blob), shaped, uploaded[slot]
 
-    def run(k0, n):
-        nonlocal h2d, d2h
-        b_in = upload(k0)
-        for k in range(k0, k0 + n):
-            slot = k % 2
-            if k + 1 < k0 + n:
-                nxt = upload(k + 1)
-            stream.wait_event(path._ready[k % R])
-            p = path._ring[k % R]
-            i = k % n_distinct
-            shaped = [dev_ar[slot][g][: host_ar[i][g].numel()].view(host_ar[i][g].shape)
-                      for g in range(2)]
-            path.dispatch(p, shaped, stream)
-            ev = path.return_scatter(p, stream)
-            path._freed[k % R] = ev
-            stream.wait_event(ev)
-            out_hdr[slot].copy_(p.view("header", _lib.H_SLOTS), non_blocking=True)
-            c = torch.cuda.Event()
-            c.record(stream)
-            consumed[slot] = c
-            h2d += b_in
-            d2h += 8 * _lib.H_SLOTS
-            if k + 1 < k0 + n:
-                b_in = nxt
+    def after(k, p, s):
+        """Read the step's plan header back (D2H) and release its input slot."""
+        slot = k % 2
+        out_hdr[slot].copy_(p.view("header", _lib.H_SLOTS), non_blocking=True)
+        c = torch.cuda.Event()
+        c.record(s)
+        consumed[slot] = c
+        counts["d2h"] += 8 * _lib.H_SLOTS
 
-    h2d = d2h = 0
-    run(0, 3)
+    def run(n):
+        path.run_pipeline(n=n, prepare=prepare, after_step=after, stream=stream)
+
+    run(3)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    h2d = d2h = 0
+    counts.update(h2d=0, d2h=0)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     up.wait_event(t0)
-    run(0, steps)
+    run(steps)
     path.finish(stream)
     t1.record(stream)
     torch.cuda.synchronize()
@@ -606,8 +588,9 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
         ms = float(tt.item())
     assert all(int(h[_lib.H_STATUS]) == 0 for h in out_hdr)
     M = sum(plans_info[k % n_distinct]["M"] for k in range(steps))
-    return {"value": M / (ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d // steps,
-            "d2h_bytes_per_step": d2h // steps, "steps": steps, "ms_per_step": ms / steps,
+    return {"value": M / (ms / 1e3), "unit": "tokens/s",
+            "h2d_bytes_per_step": counts["h2d"] // steps,
+            "d2h_bytes_per_step": counts["d2h"] // steps, "steps": steps, "ms_per_step": ms / steps,
             "note": "per step: step table + loader payload H2D from pinned host memory (copy "
                     "stream, one step ahead) and the plan header D2H, all inside the window"}
 

@@ -263,9 +263,14 @@ class MuxPath:
         self._ready[slot].record(side)
         return p
 
-    def run_pipeline(self, steps, *, encoder=None, after_step=None, kernel_events=None,
-                     start_event=None, stream=None):
+    def run_pipeline(self, steps=None, *, n=None, prepare=None, encoder=None, after_step=None,
+                     kernel_events=None, start_event=None, stream=None):
         """Run consecutive steps [(DeviceTable, arenas), ...] pipelined on `stream`.
+
+        Streaming inputs: instead of `steps`, pass `n` and `prepare(k)` returning
+        (DeviceTable, arenas, event or None); it is called once per step, one step
+        ahead (before step k-1's work is issued), e.g. to upload step k from pinned
+        host memory on a copy stream; the event orders the plan after that upload.
 
         The plan of step k+1 runs on the planner's side stream during step k;
         with overlap_dispatch, step k+1's dispatch also runs (copy stream) under
@@ -275,32 +280,47 @@ class MuxPath:
         stream) after the return.  kernel_events[k]: (start, end) events around
         step k's return kernel."""
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
-        n, R = len(steps), self.RING
+        if steps is not None:
+            n = len(steps)
+            fixed = {k: (steps[k][0], steps[k][1], None) for k in range(n)}
+            get = fixed.__getitem__
+        else:
+            cache: dict = {}
+
+            def get(k):
+                if k not in cache:
+                    cache[k] = prepare(k)
+                return cache[k]
+        R = self.RING
         if not n:
             return
         self._ensure_ring()
         base = getattr(self, "_kstep", 0)
         slot = [(base + k) % R for k in range(n)]
         ov = self.overlap_dispatch
-        self.plan_ahead(steps[0][0], slot[0], after=start_event)
+        d0, a0, e0 = get(0)
+        if e0 is not None and start_event is not None:
+            self._side.wait_event(start_event)
+        self.plan_ahead(d0, slot[0], after=e0 if e0 is not None else start_event)
         if ov:
             if getattr(self, "_copy", None) is None:
                 self._copy = torch.cuda.Stream(self.device)
                 self._dispatched = [_event() for _ in range(R)]
             cs = self._copy
             cs.wait_event(self._ready[slot[0]])
-            self.dispatch(self._ring[slot[0]], steps[0][1], cs)
+            self.dispatch(self._ring[slot[0]], a0, cs)
             self._dispatched[slot[0]].record(cs)
         for k in range(n):
             s = slot[k]
             if k + 1 < n:
-                self.plan_ahead(steps[k + 1][0], slot[k + 1])
+                dn, _, en = get(k + 1)
+                self.plan_ahead(dn, slot[k + 1], after=en)
             p = self._ring[s]
             if ov:
                 main.wait_event(self._dispatched[s])
             else:
                 main.wait_event(self._ready[s])
-                self.dispatch(p, steps[k][1], main)
+                self.dispatch(p, get(k)[1], main)
             if encoder is not None:
                 encoder(k, p, main)
             if ov:
@@ -315,7 +335,7 @@ class MuxPath:
                 # every rank's "consumed" signal (carried by that kernel) must never
                 # sit in front of it in a shared hardware queue
                 cs.wait_event(self._ready[slot[k + 1]])
-                self.dispatch_overlapped(self._ring[slot[k + 1]], steps[k + 1][1], cs, after=ev)
+                self.dispatch_overlapped(self._ring[slot[k + 1]], get(k + 1)[1], cs, after=ev)
                 self._dispatched[slot[k + 1]].record(cs)
             if after_step is not None:
                 after_step(k, p, main)

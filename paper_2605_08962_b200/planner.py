@@ -113,6 +113,23 @@ class DeviceTable:
         self.carry_seq = i32 + 8 * S
         self.chunk_off = i32 + 4 * (2 * S + nc)
 
+    @classmethod
+    def from_blob(cls, table: StepTable, blob: torch.Tensor) -> "DeviceTable":
+        """A view of a step-table blob already on the device (e.g. uploaded by a
+        loader on its own stream): no copy."""
+        return _device_table_from_blob(table, blob)
+
+
+def _device_table_from_blob(table: StepTable, blob: torch.Tensor) -> "DeviceTable":
+    dt = DeviceTable.__new__(DeviceTable)
+    dt.table, dt.blob = table, blob
+    S, nc = table.S, table.n_carry
+    base = blob.data_ptr()
+    dt.ids = base
+    dt.lens, dt.mods = base + 8 * S, base + 12 * S
+    dt.carry_seq, dt.chunk_off = base + 16 * S, base + 16 * S + 4 * nc
+    return dt
+
 
 def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int = 1,
              world: int = 1, mbs: int = 1, method: str = "lpt", pooled: bool = False,
