@@ -308,7 +308,8 @@ class MuxPath:
                 self._dispatched = [_event() for _ in range(R)]
             cs = self._copy
             cs.wait_event(self._ready[slot[0]])
-            self.dispatch(self._ring[slot[0]], a0, cs)
+            # waits for every peer's last "consumed" signal of an earlier call too
+            self.dispatch_overlapped(self._ring[slot[0]], a0, cs)
             self._dispatched[slot[0]].record(cs)
         for k in range(n):
             s = slot[k]
