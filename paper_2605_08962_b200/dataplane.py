@@ -80,6 +80,17 @@ class MuxPath:
           has fired and stay valid until step k+2's projector runs); the
           owners' rows are not balanced by the encoder-side LPT, so at 2 GPUs it
           measured no faster than "fused".
+
+    Other options:
+      method            encoder balancing: "lpt_local" (bench default), "lpt",
+                        "kk", "lpt_local_rw";
+      lssp_eta/lssp_sp  LSSP eta split: longer samples are encoded as token
+                        shards over groups of lssp_sp ranks (None: off);
+      reshard           LLM placement over each replica's sp ranks: "ulysses"
+                        or "cp_hybrid" (cp_threshold, 0 = capacity / sp);
+      text_embed        also emit text segments for `embed_text`;
+      overlap_dispatch  `run_pipeline` dispatches step k+1 under step k's
+                        return (E/D/R flag channels, alternating LLM buffers).
     """
 
     def __init__(self, *, capacity: int, gbs: int, dp: int, sp: int = 1, world: int = 1,
