@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--distinct", type=int, default=8, help="distinct step inputs cycled")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-nested", action="store_true",
+                    help="skip the nested north-star record (target1 at 1 GPU, cfg5 at N>1)")
+    ap.add_argument("--no-comparator", action="store_true",
+                    help="skip the cuBLAS + index_copy_ comparator of the projector")
     ap.add_argument("--stages", action="store_true", help="per-stage timing breakdown")
     ap.add_argument("--pipeline", type=int, default=2,
                     help="1: plan step k+1 on a side stream during step k; 2 (default): also "
@@ -84,23 +88,6 @@ def exchange_summary(plans_info, steps_idx, rank):
             "dispatch_remote_frac": avg["disp_remote"] / max(avg["disp_bytes"], 1),
             "return_bytes": avg["ret_bytes"],
             "return_remote_frac": avg["ret_remote"] / max(avg["ret_bytes"], 1)}
-
-
-def measured_traffic(name, algo_bytes):
-    """DRAM bytes per launch of the dominant kernel: the ncu-captured launch's
-    traffic/algorithmic ratio (profiles/traffic.json) applied to this run's
-    algorithmic bytes per launch.  (None, why) when no capture exists."""
-    try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                               "traffic.json")) as f:
-            rec = json.load(f).get(name)
-    except (OSError, ValueError):
-        rec = None
-    if not rec:
-        return None, f"no ncu capture for {name} in profiles/traffic.json"
-    ratio = (rec["dram_read"] + rec["dram_write"]) / rec["algorithmic_bytes"]
-    return algo_bytes * ratio, (f"ncu --set full, {rec['summary']}: dram r+w / algorithmic "
-                                f"= {ratio:.3f} on the captured launch, scaled")
 
 
 def workload(name, world):
@@ -233,13 +220,47 @@ def peaks():
 # our arm
 # ----------------------------------------------------------------------------
 
+def choose_tensor_peak(clocks):
+    """Burst or sustained bf16 denominator from the run's own clock record:
+    sustained only when the GPU was power-capped (sw_power_cap seen) or its
+    median SM clock sat below 0.9x max; otherwise the burst figure."""
+    hbm, burst, sus, src = peaks()
+    reasons = (clocks or {}).get("reasons") or []
+    med, mx = (clocks or {}).get("sm_mhz"), (clocks or {}).get("sm_max_mhz")
+    capped = "sw_power_cap" in reasons or (med is not None and mx and med < 0.9 * mx)
+    if capped:
+        return sus, (f"bf16_tflops_sustained ({src}): sw_power_cap or median clock < 0.9x max "
+                     f"in this run's record; burst {burst}")
+    return burst, (f"bf16_tflops burst ({src}): median clock {med} of max {mx} MHz, no power "
+                   f"cap in this run's record; sustained {sus}")
+
+
+def config_dict(name, world, n_distinct, M_per_step, T_per_step):
+    """The `config` both arms print (identical for the same flags)."""
+    from paper_2605_08962_b200 import configs
+    cfg, dp, sp, gbs = workload(name, world)
+    return {"workload": name, "global_batch": gbs, "seq_len": configs.CAPACITY,
+            "parallelism": f"enc dp{world} / llm dp{dp} sp{sp}",
+            "projector": bool(cfg["projector"]), "d_in": list(configs.D_IN),
+            "d_enc": list(configs.D_ENC), "d_llm": configs.D_LLM,
+            "distinct_steps": n_distinct, "modality_tokens_per_step": M_per_step,
+            "llm_tokens_per_step": T_per_step,
+            "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"}
+
+
+def n_distinct_of(args):
+    return max(1, min(args.distinct, args.steps + args.warmup))
+
+
+def timed_indices(args, n_distinct):
+    return [(args.warmup + k) % n_distinct for k in range(args.steps)]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2605_08962_b200 import _lib, build as B, configs
-    from paper_2605_08962_b200.dataplane import MuxPath
-    from paper_2605_08962_b200.planner import DeviceTable
+    from paper_2605_08962_b200 import _lib, build as B
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -258,12 +279,41 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
     _lib.lib()
+    ctx = dict(world=world, rank=rank, local=local, dev=dev, group=group)
 
-    name = args.config
+    line = measure(args.config, args, ctx, primary=True)
+    # the north-star records beside the headline, in the same process: target-1
+    # (projector off, bit-exact, HBM roofline) at one GPU; the phase-cycling
+    # mixed batch (projector off, NVLink roofline) across GPUs
+    if not args.no_nested:
+        nested = "target1" if world == 1 else "cfg5"
+        if nested != args.config:
+            sub = measure(nested, args, ctx, primary=False)
+            for k in ("metric", "unit", "higher_is_better", "dtype", "data", "vs_baseline",
+                      "n_gpus", "steps", "warmup", "scaling"):
+                sub.pop(k, None)
+            line[nested] = sub
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure(name, args, ctx, primary=True):
+    """One workload through the pipelined step loop; returns its JSON record."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_08962_b200 import _lib, configs
+    from paper_2605_08962_b200.dataplane import MuxPath
+    from paper_2605_08962_b200.planner import DeviceTable
+
+    world, rank, local, dev, group = (ctx[k] for k in ("world", "rank", "local", "dev", "group"))
     cfg, dp, sp, gbs = workload(name, world)
     projector = bool(cfg["projector"])
     d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, configs.D_LLM
-    n_distinct = max(1, min(args.distinct, args.steps + args.warmup))
+    n_distinct = n_distinct_of(args)
     tables = generate_steps(name, world, n_distinct)
 
     path = MuxPath(capacity=configs.CAPACITY, gbs=gbs, dp=dp, sp=sp, world=world, rank=rank,
@@ -294,6 +344,13 @@ def run_ours(args):
                           generator=gen).to(torch.bfloat16) for g in range(2)]
         dtabs.append(dt)
         arenas.append(ar)
+        # return bytes of this rank per destination rank (NVLink accounting)
+        ret_to = np.zeros(world)
+        for (_s, _d, rows, g, r) in info["rseg"]:
+            ret_to[int(r)] += int(rows) * 2 * path.d_ret[int(g)]
+        disp_to = np.zeros(world)
+        for (_s, _d, rows, g, r) in info["dseg"]:
+            disp_to[int(r)] += int(rows) * 2 * d_in[int(g)]
         m_tokens = int(info["recv_rows"].sum())  # modality tokens of the whole batch
         plans_info.append(dict(M=m_tokens, T=int(info["llm_rows"].sum()),
                                S=int(h[_lib.H_N_BATCH]),
@@ -301,7 +358,8 @@ def run_ours(args):
                                disp_bytes=int(h[_lib.H_DISPATCH_BYTES]),
                                ret_bytes=int(h[_lib.H_RETURN_BYTES]),
                                disp_remote=int(h[_lib.H_DISPATCH_REMOTE]),
-                               ret_remote=int(h[_lib.H_RETURN_REMOTE])))
+                               ret_remote=int(h[_lib.H_RETURN_REMOTE]),
+                               ret_to=ret_to, disp_to=disp_to))
     text_tokens, text_table = [], None
     if args.text_embed:  # synthetic token ids per distinct step, a 32K-row embedding table
         text_table = torch.randn(32000, d_llm, device=dev).to(torch.bfloat16)
@@ -384,10 +442,15 @@ def run_ours(args):
     path.check_wait()
     ms = t0.elapsed_time(t1)
 
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
+    def max_over_ranks(x):
+        if world == 1:
+            return float(x)
+        tt = torch.tensor([float(x)], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        return float(tt.item())
+
+    ms = max_over_ranks(ms)
+    if world > 1:
         dist.barrier()
 
     # per-stage breakdown (separate untimed pass, CUDA events between stages)
@@ -411,6 +474,7 @@ def run_ours(args):
             path.grad_return(p, dy, stream)
         ev[k][4].record(stream)
     torch.cuda.synchronize()
+    path.check_wait()
     stages = {nm: float(np.mean([e[j].elapsed_time(e[j + 1]) for e in ev]))
               for j, nm in enumerate(("plan_ms", "pack_dispatch_ms",
                                       "projector_scatter_ms" if projector else "return_scatter_ms",
@@ -424,34 +488,46 @@ def run_ours(args):
     M_total = sum(plans_info[i]["M"] for i in steps_idx)
     T_total = sum(plans_info[i]["T"] for i in steps_idx)
     value = M_total / (ms / 1e3)
+    clocks = clk.summary() if rank == 0 else None
+    if world > 1:  # every rank picks the same denominator: rank 0's clock record
+        obj = [clocks]
+        dist.broadcast_object_list(obj, src=0)
+        clocks = obj[0]
 
     # dominant kernel roofline (rank-local)
-    hbm, tf_burst, tf_sus, src = peaks()
+    hbm, _, _, src = peaks()
     dom_avg_s = float(np.mean(dom_ms)) / 1e3
     my_recv = [sum(plans_info[i]["recv"][g] for i in steps_idx) / len(steps_idx) for g in (0, 1)]
     if projector:
         from paper_2605_08962_b200 import costs
+        tf_peak, peak_why = choose_tensor_peak(clocks)
         flops = sum(costs.projector_flops(my_recv[g], d_enc[g], d_llm) for g in (0, 1))
         algo_bytes = sum(my_recv[g] * 2 * (d_enc[g] + d_llm) + 2 * d_enc[g] * d_llm
                          for g in (0, 1) if my_recv[g] > 0)
         roof = {"kernel": "proj_scatter_gemm (tcgen05)", "bound": "tensor",
-                "achieved": flops / dom_avg_s / 1e12, "peak": tf_sus, "unit": "TFLOP/s",
-                "peak_source": f"bf16_tflops_sustained ({src}): the GEMM runs inside a long "
-                               f"step loop; burst {tf_burst}"}
+                "achieved": flops / dom_avg_s / 1e12, "peak": tf_peak, "unit": "TFLOP/s",
+                "peak_source": peak_why, "flops_per_launch": flops}
     else:
         ret = sum(plans_info[i]["ret_bytes"] for i in steps_idx) / len(steps_idx)
         algo = 2 * ret  # read + write of every returned row
         algo_bytes = algo
-        bound = "hbm" if world == 1 else "nvlink"
         roof = {"kernel": "segcopy return+scatter", "bound": "hbm",
                 "achieved": algo / dom_avg_s / 1e9, "peak": hbm, "unit": "GB/s",
-                "peak_source": f"hbm_gbs ({src})"}
-        if bound == "nvlink":
-            roof["note"] = "N>1: rows cross NVLink; HBM figure shown for the local side"
+                "peak_source": f"hbm_gbs ({src}); nominal 8000 GB/s",
+                "frac_of_nominal_8000": algo / dom_avg_s / 1e9 / 8000.0}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["algorithmic_bytes"] = algo_bytes
-    roof["traffic"], roof["traffic_source"] = measured_traffic(args.config, algo_bytes)
+    roof["traffic"], roof["traffic_source"] = captured_traffic(name)
     roof["dominant_ms"] = dom_avg_s * 1e3
+    if world > 1:
+        roof["nvlink"] = nvlink_roofline(path, plans_info, steps_idx, dom_avg_s,
+                                         stages["pack_dispatch_ms"], ctx, projector)
+    if world > 1 and not projector:  # the exchange is the bottleneck: NVLink is the bound
+        roof["hbm_side"] = {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac")}
+        nv = roof["nvlink"]
+        roof.update(bound="nvlink", achieved=nv["return"]["gbs"], peak=nv["peak_gbs"],
+                    unit="GB/s", frac=nv["return"]["frac_of_peak"],
+                    peak_source=nv["peak_source"])
 
     # e2e: public API from pinned host buffers, H2D + D2H inside the timed region
     e2e = None
@@ -477,22 +553,18 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (reference generator restated; bf16 N(0,1) payload; encoder stand-in)",
-        "config": {"workload": name, "global_batch": gbs, "seq_len": configs.CAPACITY,
-                   "parallelism": f"enc dp{world} / llm dp{dp} sp{sp}",
-                   "projector": projector, "d_in": list(d_in), "d_enc": list(d_enc),
-                   "d_llm": d_llm, "distinct_steps": n_distinct,
-                   "modality_tokens_per_step": M_total / args.steps,
-                   "planner": ("pipelined on a side stream" if args.pipeline else "in-line") +
-                              ("; dispatch of step k+1 under step k's return"
-                               if args.pipeline >= 2 else ""),
-                   "balance": args.method,
-                   "lssp": ({"eta": args.lssp_eta, "group": args.lssp_sp or world}
-                            if args.lssp_eta >= 0 else None),
-                   "reshard": args.reshard if sp > 1 else None,
-                   "text_rows": bool(args.text_embed),
-                   "launch": "one CUDA graph per step" if graphs is not None else "eager",
-                   "llm_tokens_per_step": T_total / args.steps,
-                   "l2": "per-step working set > 126 MB L2 (inputs larger than L2)"},
+        "config": config_dict(name, world, n_distinct, M_total / args.steps,
+                              T_total / args.steps),
+        "impl_config": {
+            "planner": ("pipelined on a side stream" if args.pipeline else "in-line") +
+                       ("; dispatch of step k+1 under step k's return"
+                        if args.pipeline >= 2 else ""),
+            "balance": args.method,
+            "lssp": ({"eta": args.lssp_eta, "group": args.lssp_sp or world}
+                     if args.lssp_eta >= 0 else None),
+            "reshard": args.reshard if sp > 1 else None,
+            "text_rows": bool(args.text_embed),
+            "launch": "one CUDA graph per step" if graphs is not None else "eager"},
         "roofline": roof,
         "exchange": exchange_summary(plans_info, steps_idx, rank),
         "stages": stages,
@@ -500,14 +572,215 @@ def run_ours(args):
         "host_enqueue_ms_per_step": host_ms / args.steps,
         "e2e": e2e,
     }
+    if projector and world == 1 and not args.no_comparator:
+        line["comparator"] = library_comparator(path, dtabs, steps_idx, dom_avg_s * 1e3, stream)
     if rank == 0:
-        line["clocks"] = clk.summary()
+        line["clocks"] = clocks
         if world == 1:
             line["cpu_baseline"] = cpu_baseline(name, tables[0], projector, world, args.method)
-        print(json.dumps(line), flush=True)
-    if world > 1:
+    return line
+
+
+def nvlink_roofline(path, plans_info, steps_idx, ret_s, disp_ms, ctx, projector):
+    """Per-GPU NVLink bandwidth of the two exchanges at N > 1.
+
+    Bytes: each rank's return (and dispatch) bytes per destination rank from
+    its plan, averaged over the timed steps and all-gathered into the world's
+    byte matrix; per rank egress = row sum off the diagonal, ingress = column
+    sum.  Time: the exchange kernel's CUDA-event duration, max over ranks.
+    Achieved = max over ranks of max(egress, ingress) / that time, the per-GPU
+    roofline of SURVEY §8(d).  Peaks measured in this run on the same windows:
+    a ring push by the same copy engine (SM stores to the next rank) and the
+    copy engine (cudaMemcpyAsync to the peer); NCCL all_to_all_single on the
+    same byte matrix is the library comparator."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, dev = ctx["world"], ctx["rank"], ctx["dev"]
+    n = len(steps_idx)
+    mine_ret = sum(plans_info[i]["ret_to"] for i in steps_idx) / n
+    mine_disp = sum(plans_info[i]["disp_to"] for i in steps_idx) / n
+
+    def gather(vec):
+        t = torch.tensor(vec, dtype=torch.float64, device=dev)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return np.stack([o.cpu().numpy() for o in out])
+
+    def gmax(x):
+        t = torch.tensor([float(x)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    Rm, Dm = gather(mine_ret), gather(mine_disp)
+    ret_ms, disp_ms = gmax(ret_s * 1e3), gmax(disp_ms)
+    probe = nvlink_probe(path, ctx)
+
+    def rec(Mx, t_ms):
+        off = Mx - np.diag(np.diag(Mx))
+        eg, ing = off.sum(1), off.sum(0)
+        b = float(max(eg.max(), ing.max()))
+        gbs = b / (t_ms / 1e3) / 1e9 if t_ms > 0 else 0.0
+        return {"remote_bytes_max_rank": b, "egress_bytes": eg.tolist(),
+                "ingress_bytes": ing.tolist(), "local_bytes": np.diag(Mx).tolist(),
+                "exchange_ms": t_ms, "gbs": gbs, "frac_of_peak": gbs / probe["peak_gbs"],
+                "frac_of_900": gbs / 900.0}
+
+    out = {"return": rec(Rm, ret_ms),
+           "dispatch": rec(Dm, disp_ms),
+           "peak_gbs": probe["peak_gbs"],
+           "peak_source": probe["peak_source"],
+           "probe": probe,
+           "nominal_gbs": 900.0,
+           "note": "return: the kernel timed in the step loop (projector: the GEMM whose "
+                   "epilogue stores remote rows); dispatch: the pack+dispatch stage of the "
+                   "in-line stage pass (includes its flag wait)"}
+    out["nccl_all_to_allv"] = nccl_comparator(Rm, ctx)
+    out["return"]["vs_nccl"] = out["nccl_all_to_allv"]["ms"] / ret_ms if ret_ms else None
+    return out
+
+
+def nvlink_probe(path, ctx, nbytes=256 << 20, iters=5):
+    """Ring push of `nbytes` from every rank to rank+1's receive window: SM
+    stores (mux_copy_bytes, the exchange's copy engine) and the copy engine
+    (cudaMemcpyAsync to the peer pointer).  Max over ranks of CUDA-event time."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_08962_b200 import _lib
+    world, rank, dev = ctx["world"], ctx["rank"], ctx["dev"]
+    win = path.recv[0]
+    nbytes = min(nbytes, win.tensor.numel()) & ~((1 << 20) - 1)
+    src = torch.empty(nbytes, dtype=torch.uint8, device=dev).fill_(rank)
+    dst = win.ptrs[(rank + 1) % world]
+    L = _lib.lib()
+    s = torch.cuda.current_stream()
+    res = {}
+    for nm, fn in (("sm_push_ring", lambda: L.mux_copy_bytes(C.c_void_p(dst),
+                                                                C.c_void_p(src.data_ptr()),
+                                                                nbytes, 0, C.c_void_p(s.cuda_stream))),
+                   ("copy_engine_ring", lambda: L.mux_memcpy_async(C.c_void_p(dst),
+                                                                   C.c_void_p(src.data_ptr()),
+                                                                   nbytes,
+                                                                   C.c_void_p(s.cuda_stream)))):
+        _lib.check(fn(), nm)
+        torch.cuda.synchronize()
         dist.barrier()
-        dist.destroy_process_group()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(iters):
+            _lib.check(fn(), nm)
+        b.record(s)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / iters], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        res[nm + "_gbs"] = nbytes / (float(t.item()) / 1e3) / 1e9
+        dist.barrier()
+    res["bytes"] = nbytes
+    res["peak_gbs"] = max(res["sm_push_ring_gbs"], res["copy_engine_ring_gbs"])
+    res["peak_source"] = ("measured in this run: best of SM-store ring push and copy-engine "
+                          "ring push, 1 peer per rank, per direction")
+    return res
+
+
+def nccl_comparator(Mx, ctx, iters=5):
+    """NCCL all_to_all_single with the exchange's byte matrix (row = sender,
+    column = receiver; the diagonal is the local part, as in our kernel)."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, dev = ctx["world"], ctx["rank"], ctx["dev"]
+    sizes = np.rint(Mx).astype(np.int64)
+    send = [int(x) for x in sizes[rank]]
+    recv = [int(sizes[s, rank]) for s in range(world)]
+    inp = torch.empty(max(sum(send), 1), dtype=torch.uint8, device=dev)
+    out = torch.empty(max(sum(recv), 1), dtype=torch.uint8, device=dev)
+    if sum(send) == 0 and sum(recv) == 0:
+        return {"ms": 0.0}
+    for _ in range(2):
+        dist.all_to_all_single(out[:sum(recv)], inp[:sum(send)], recv, send)
+    torch.cuda.synchronize()
+    dist.barrier()
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(iters):
+        dist.all_to_all_single(out[:sum(recv)], inp[:sum(send)], recv, send)
+    b.record(s)
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / iters], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    off = sizes - np.diag(np.diag(sizes))
+    b_max = float(max(off.sum(1).max(), off.sum(0).max()))
+    return {"ms": ms, "gbs": b_max / (ms / 1e3) / 1e9 if ms > 0 else 0.0,
+            "what": "torch.distributed.all_to_all_single (NCCL) of the same per-rank byte "
+                    "matrix into contiguous buffers, max over ranks"}
+
+
+def library_comparator(path, dtabs, steps_idx, fused_ms, stream, reps=None):
+    """Same-shape library path for the fused projector + scatter: cuBLAS
+    (torch.matmul) into a temporary, + bias, then index_copy_ of the rows into
+    the packed LLM buffer, on the same steps' encoder rows and row maps."""
+    import torch
+
+    from paper_2605_08962_b200 import _lib
+    reps = reps or len(steps_idx)
+    jobs = []
+    for i in sorted(set(steps_idx)):
+        p = path.plan(dtabs[i], stream)
+        h = p.header()
+        rmap = torch.empty_like(path.row_dst)
+        path._row_map(p, rmap, stream)
+        for g in range(2):
+            m = int(h[_lib.H_RECV_ROWS0 + g])
+            if m and path.weight[g] is not None:
+                idx = (rmap[g * path.max_rows: g * path.max_rows + m] & ((1 << 40) - 1))
+                jobs.append((i, g, m, idx))
+    torch.cuda.synchronize()
+    llm = path.llm_view()
+    by_step = {}
+    for (i, g, m, idx) in jobs:
+        by_step.setdefault(i, []).append((g, m, idx))
+
+    def one(i):
+        for (g, m, idx) in by_step.get(i, []):
+            x = path.enc_view(g, m)
+            y = torch.addmm(path.bias[g], x, path.weight[g].t())
+            llm.index_copy_(0, idx, y)
+
+    for i in steps_idx[:3]:
+        one(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for k in range(reps):
+        one(steps_idx[k % len(steps_idx)])
+    b.record(stream)
+    torch.cuda.synchronize()
+    lib_ms = a.elapsed_time(b) / reps
+    return {"library": "torch.addmm (cuBLAS, bf16) + index_copy_ into the packed LLM rows",
+            "library_ms": lib_ms, "fused_ms": fused_ms, "speedup": lib_ms / fused_ms}
+
+
+def captured_traffic(name):
+    """DRAM bytes (read + write) of one launch of the dominant kernel from an
+    `ncu --set full` capture (profiles/traffic.json), or (None, why).  The
+    captured launch's own algorithmic bytes are named in the source string:
+    compare ratios, since the captured step may differ from the timed mix."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            rec = json.load(f).get(name)
+    except (OSError, ValueError):
+        rec = None
+    if not rec:
+        return None, f"no ncu capture for {name} in profiles/traffic.json"
+    t = rec["dram_read"] + rec["dram_write"]
+    return t, (f"ncu --set full of one launch ({rec['summary']}; {rec['launch']}): dram r+w "
+               f"{t} B vs that launch's algorithmic {rec['algorithmic_bytes']} B "
+               f"(ratio {t / rec['algorithmic_bytes']:.3f})")
 
 
 def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, world):
@@ -558,8 +831,12 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
         return DeviceTable.from_blob(tables[i], blob), shaped, uploaded[slot]
 
     def after(k, p, s):
-        """Read the step's plan header back (D2H) and release its input slot."""
+        """Read the step's plan header back (D2H) and release its input slot once
+        every reader of the step's inputs ran (path.step_done: the event after
+        which the step's plan and inputs are no longer read)."""
         slot = k % 2
+        if path.step_done is not None:
+            s.wait_event(path.step_done)
         out_hdr[slot].copy_(p.view("header", _lib.H_SLOTS), non_blocking=True)
         c = torch.cuda.Event()
         c.record(s)
@@ -571,6 +848,7 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
 
     run(3)
     torch.cuda.synchronize()
+    path.check_wait()
     if world > 1:
         dist.barrier()
     counts.update(h2d=0, d2h=0)
@@ -581,6 +859,7 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
     path.finish(stream)
     t1.record(stream)
     torch.cuda.synchronize()
+    path.check_wait()
     ms = t0.elapsed_time(t1)
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -596,19 +875,70 @@ def run_e2e(args, path, tables, arenas, plans_info, n_distinct, projector, dev, 
 
 
 # ----------------------------------------------------------------------------
-# CPU reference arm (oracle port; the reference itself never moves token data)
+# CPU reference arm (the reference's own packer + the oracle port of the
+# SPEC-only balance/reshard and of the data plane; the reference itself never
+# moves token data)
 # ----------------------------------------------------------------------------
 
-def cpu_baseline(name, table, projector, world=1, method="lpt_local"):
-    """Time the CPU port on one step of the workload at `world` GPUs' scale.
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
-    Code timed: the oracle planner (FFD + batch + LPT + reshard; restates the
-    reference's hybrid_pack / build_global_batch, workload.py:240-278) and the
-    data plane in torch-CPU over all ranks' rows at once (index_select pack,
-    index_copy_ return/scatter; the projector as an fp32 matmul timed on a
-    4096-row slice and extrapolated).  All host threads.  One step = the bounded
-    sample.
-    """
+
+def _reference_workload():
+    """The reference's own muxsim.workload from baseline/_ref (installed from
+    /root/reference/pkg), or None when it is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "muxsim")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import muxsim.workload as RW
+        return RW
+    except Exception:
+        return None
+
+
+def reference_pack(RW, table, capacity):
+    """The reference's hybrid_pack on every drawn chunk of the step table (its
+    own code, workload.py:240-262) after the carried sequences, then its
+    build_global_batch is left to the caller.  Returns (sequences, seconds)
+    with only the hybrid_pack calls inside the timing."""
+    mods = {0: "text", 1: "image", 2: "video", 3: "audio"}
+    lens, ids, tmods = table["lens"], table["ids"], table["mods"]
+    nc = len(table["carry_seq"])
+    seqs = [RW.PackedSequence(capacity=capacity) for _ in range(int(table["n_carry_seqs"]))]
+    for i in range(nc):
+        seqs[int(table["carry_seq"][i])].spans.append((int(ids[i]), int(lens[i])))
+    chunks = []
+    co = list(table["chunk_off"])
+    for c in range(len(co) - 1):
+        chunks.append([RW.Sample(int(ids[i]), RW.Modality(mods[int(tmods[i])]), "synthetic",
+                                 int(lens[i])) for i in range(co[c], co[c + 1])])
+    t0 = time.perf_counter()
+    for ch in chunks:
+        seqs.extend(RW.hybrid_pack(ch, capacity))
+    return seqs, time.perf_counter() - t0
+
+
+def cpu_baseline(name, table, projector, world=1, method="lpt_local", weights=None):
+    """Time the CPU path on one step of the workload at `world` GPUs' scale.
+
+    Code timed: the reference's own hybrid_pack + build_global_batch from
+    baseline/_ref (workload.py:240-278; the oracle restatement when that is
+    absent), the oracle port of the SPEC-only balance / reshard / segment
+    tables, and the data plane in torch-CPU over all ranks' rows at once
+    (index_select pack, index_copy_ return/scatter, and the projector as an
+    fp32-accumulate matmul over every row).  All host threads.  One step = the
+    bounded sample."""
     import torch
 
     from oracle import planner as oplan
@@ -621,9 +951,21 @@ def cpu_baseline(name, table, projector, world=1, method="lpt_local"):
              carry_seq=table.carry_seq.astype(np.int64), n_carry_seqs=table.n_carry_seqs,
              chunk_off=table.chunk_off.tolist())
     d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, configs.D_LLM
-    t0 = time.perf_counter()
-    o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
-    t_plan = time.perf_counter() - t0
+    RW = _reference_workload()
+    if RW is not None:
+        seqs, t_pack_ref = reference_pack(RW, t, configs.CAPACITY)
+        t0 = time.perf_counter()
+        RW.build_global_batch(seqs, 0, gbs, dp, 1)
+        packed = oplan.packed_from_sequences(t, seqs)
+        o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method, packed=packed)
+        t_plan = t_pack_ref + time.perf_counter() - t0
+        planner_kind = ("reference hybrid_pack + build_global_batch (baseline/_ref) + oracle "
+                        "balance/reshard/segments")
+    else:
+        t0 = time.perf_counter()
+        o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
+        t_plan = time.perf_counter() - t0
+        planner_kind = "oracle planner (baseline/_ref absent)"
     lens = t["lens"]
     items = np.flatnonzero(o["enc"] >= 0)
     rows = [int(o["arena_rows"][:, g].sum()) for g in range(2)]
@@ -639,6 +981,8 @@ def cpu_baseline(name, table, projector, world=1, method="lpt_local"):
     recv = [torch.empty(max(r, 1), d_in[g], dtype=torch.bfloat16) for g, r in enumerate(rows)]
     d_ret = d_enc if projector else (d_llm, d_llm)
     enc = [torch.randn(max(r, 1), d_ret[g]).to(torch.bfloat16) for g, r in enumerate(rows)]
+    Ws = [torch.randn(d_llm, d_enc[g]).to(torch.bfloat16) for g in range(2)] if projector \
+        else None
     llm = torch.zeros(int(o["llm_rows"].sum()), d_llm, dtype=torch.bfloat16)
     t0 = time.perf_counter()
     for g in range(2):  # pack + dispatch: origin arena rows -> encoder receive rows
@@ -655,8 +999,6 @@ def cpu_baseline(name, table, projector, world=1, method="lpt_local"):
             recv[g].index_copy_(0, dI, arenas[g].index_select(0, sI))
     t_pack = time.perf_counter() - t0
     t0 = time.perf_counter()
-    extra = 0.0
-    scale = 1.0
     for g in range(2):  # return (+ projector) + scatter into the packed LLM rows
         src, dst = [], []
         for (i, sr, dr_rank, dr, n) in o["pieces"]:
@@ -668,56 +1010,59 @@ def cpu_baseline(name, table, projector, world=1, method="lpt_local"):
             continue
         sI, dI = torch.from_numpy(np.concatenate(src)), torch.from_numpy(np.concatenate(dst))
         x = enc[g].index_select(0, sI)
-        if projector:
-            W = torch.randn(d_llm, d_enc[g]).to(torch.bfloat16)
-            m = min(4096, x.shape[0])
-            tg = time.perf_counter()
-            y = (x[:m].float() @ W.float().t()).to(torch.bfloat16)
-            tm = time.perf_counter() - tg
-            scale = x.shape[0] / m
-            extra += tm * (scale - 1)  # the remaining rows, extrapolated
-            x = torch.cat([y, torch.zeros(x.shape[0] - m, d_llm, dtype=torch.bfloat16)])
+        if projector:  # every row, fp32 accumulate, rounded to bf16
+            x = (x.float() @ Ws[g].float().t()).to(torch.bfloat16)
         llm.index_copy_(0, dI, x)
-    t_ret = time.perf_counter() - t0 + extra
+    t_ret = time.perf_counter() - t0
     M = int(o["recv_rows"].sum())
     total = t_plan + t_pack + t_ret
     sample = (f"one {name} step at {world} GPU(s) simulated in-process: {M} modality tokens; "
-              "oracle planner + torch-CPU gather/scatter"
-              + (f"; projector timed on 4096 rows, x{scale:.1f} extrapolated" if projector else ""))
+              f"{planner_kind}; torch-CPU gather/scatter"
+              + ("; fp32 projector over all rows" if projector else ""))
     return {"value": M / total, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": sample, "seconds": {"plan": t_plan, "pack": t_pack, "return": t_ret},
-            "step_seconds": total}
+            "cpu_model": cpu_model(), "sample": sample,
+            "seconds": {"plan": t_plan, "pack": t_pack, "return": t_ret},
+            "step_seconds": total, "M": M, "T": int(o["llm_rows"].sum())}
 
 
 def run_reference(args):
-    """CPU reference arm: rank 0 only; the other ranks exit without work."""
+    """CPU reference arm: rank 0 only; the other ranks exit without work.  The
+    same distinct steps in the same order as our arm's timed region, and the
+    same `config`."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2605_08962_b200 import configs
     name = args.config
     cfg, dp, sp, gbs = workload(name, world)
-    tables = generate_steps_host(name, world, max(1, min(args.steps + args.warmup, 4)))
+    n_distinct = n_distinct_of(args)
+    tables = generate_steps_host(name, world, n_distinct)
     vals = []
     for k in range(args.warmup + args.steps):
-        r = cpu_baseline(name, tables[k % len(tables)], bool(cfg["projector"]), world,
+        r = cpu_baseline(name, tables[k % n_distinct], bool(cfg["projector"]), world,
                          args.method)
         if k >= args.warmup:
             vals.append(r)
-    v = float(np.mean([r["value"] for r in vals]))
+    secs = sum(r["step_seconds"] for r in vals)
+    M = sum(r["M"] for r in vals)
+    v = M / secs
     line = {"metric": "multimodal tokens/s rebalanced+dispatched+scattered per step",
             "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": float(np.mean([r["step_seconds"] for r in vals])) * 1e3,
+            "warmup": args.warmup, "ms_per_step": secs / len(vals) * 1e3,
             "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference generator restated; bf16 N(0,1) payload; encoder stand-in)",
             "impl": "reference",
-            "config": {"workload": name, "global_batch": gbs, "seq_len": configs.CAPACITY,
-                       "parallelism": f"enc dp{world} / llm dp{dp} sp{sp} (simulated in-process)",
-                       "projector": bool(cfg["projector"])},
+            "config": config_dict(name, world, n_distinct, M / len(vals),
+                                  sum(r["T"] for r in vals) / len(vals)),
+            "impl_config": {"ranks": f"{world} simulated in-process on the host",
+                            "balance": args.method},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": vals[0]["cores"],
-                             "kind": "port", "sample": vals[0]["sample"]},
+                             "kind": "port", "cpu_model": vals[0]["cpu_model"],
+                             "sample": vals[0]["sample"],
+                             "seconds_per_step": {k: float(np.mean([r["seconds"][k]
+                                                                     for r in vals]))
+                                                  for k in ("plan", "pack", "return")}},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -239,11 +239,15 @@ int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int32_t which,
 /* General form: segments whose destination rank is `skip_rank` are not
  * copied (-1: copy all); flags_peers may be NULL (no completion signal).
  * grid_ctas < 0 launches -grid_ctas CTAs without shared memory, so the copy
- * can co-reside with a kernel that holds the SMs' shared memory. */
+ * can co-reside with a kernel that holds the SMs' shared memory.
+ * poison (nullable): the path's device status word, the err_dev of its
+ * mux_wait calls.  Nonzero = the step is poisoned (a flag wait timed out or
+ * saw a poisoned peer): the copy moves nothing and publishes its epoch with
+ * MUX_POISON_BIT set, so every peer's wait fails fast too. */
 int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                    void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
                    int32_t skip_rank, uint64_t* const* flags_peers, uint32_t* sync,
-                   uint64_t* epoch_ctr, void* stream);
+                   uint64_t* epoch_ctr, const int32_t* poison, void* stream);
 
 /* One contiguous 8-byte-aligned byte range with the same copy engine as
  * mux_segcopy (local or NVLink-peer dst/src); used by the NVLink probe. */
@@ -256,7 +260,9 @@ int mux_memcpy_async(void* dst, const void* src, int64_t n, void* stream);
  * advances the device epoch counter (e = ++*epoch_ctr) and stores e into
  * flag[me] of every peer after a system-scope fence; wait spins until every
  * flag[src] of `my_flags` >= *epoch_ctr (bounded: timeout_ms; a timeout sets
- * *err_dev = 1 and returns). */
+ * *err_dev = 1 and returns; a flag carrying MUX_POISON_BIT sets *err_dev = 2;
+ * a wait issued while *err_dev != 0 returns at once). */
+#define MUX_POISON_BIT (1ull << 63)
 int mux_signal(int32_t me, int32_t world, uint64_t* const* flags_peers, uint64_t* epoch_ctr,
                void* stream);
 int mux_wait(int32_t world, const uint64_t* my_flags, const uint64_t* epoch_ctr,
@@ -343,12 +349,13 @@ int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_groups, int
  * kernel re-arms.  e_flags_peers / e_epoch_ctr (optional, NULL = none): a
  * second channel signalled at kernel START without a fence — the
  * "receive windows consumed" permission (mux_signal_ex with fence 0) fused
- * into the launch. */
+ * into the launch.  poison (nullable): as for mux_segcopy_ex — a poisoned
+ * launch computes nothing and publishes its epoch with MUX_POISON_BIT. */
 int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int32_t n_groups, int32_t N,
                                     void* const* out_bases, int32_t num_sms, int32_t me,
                                     int32_t world, uint64_t* const* flags_peers, uint32_t* sync,
                                     uint64_t* epoch_ctr, uint64_t* const* e_flags_peers,
-                                    uint64_t* e_epoch_ctr, void* stream);
+                                    uint64_t* e_epoch_ctr, const int32_t* poison, void* stream);
 
 #ifdef __cplusplus
 }

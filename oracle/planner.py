@@ -135,10 +135,14 @@ def ulysses_split(fill, sp):
 # step plan
 # ----------------------------------------------------------------------------
 
-def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=False):
+def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=False,
+              packed=None):
     """Plan one step.  `table` dict: lens, mods, ids (arrays over S samples),
     carry_seq (array over the first n_carry samples: their carry sequence),
-    n_carry_seqs, chunk_off (offsets of drawn chunks, first = n_carry)."""
+    n_carry_seqs, chunk_off (offsets of drawn chunks, first = n_carry).
+    packed: optional (seq, off, span, fills) of an FFD placement computed
+    elsewhere — bench.py's reference arm passes the reference's own
+    hybrid_pack output (packed_from_sequences) and times only the rest here."""
     lens = np.asarray(table["lens"], dtype=np.int64)
     mods = np.asarray(table["mods"], dtype=np.int64)
     ids = np.asarray(table["ids"], dtype=np.int64)
@@ -156,6 +160,20 @@ def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=F
             raise OraclePackingError(
                 f"sample {ids[i]} ({lens[i]} tokens) exceeds capacity {capacity}")
 
+    if packed is not None:
+        seq, off, span, fills = (np.asarray(a, np.int64) for a in packed)
+        fills = fills.tolist()
+        n_seq = len(fills)
+    else:
+        seq, off, span, fills, n_seq = _ffd_table(lens, ids, carry_seq, n_carry_seqs, chunk_off,
+                                                  capacity)
+    return _plan_packed(lens, mods, ids, seq, off, span, fills, n_seq, capacity, gbs, dp, sp,
+                        world, mbs, method, pooled)
+
+
+def _ffd_table(lens, ids, carry_seq, n_carry_seqs, chunk_off, capacity):
+    """Carry spans, then FFD of every drawn chunk (workload.py:240-262, :288)."""
+    S, nc = len(lens), len(carry_seq)
     seq = np.full(S, -1, np.int64)
     off = np.zeros(S, np.int64)
     span = np.zeros(S, np.int64)
@@ -186,8 +204,33 @@ def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=F
             fills[q] = bf[b]
             nspan[q] += 1
         base += len(bf)
-    n_seq = base
+    return seq, off, span, fills, base
 
+
+def packed_from_sequences(table, sequences):
+    """(seq, off, span, fills) of a list of PackedSequences (carry first, then
+    every chunk's hybrid_pack output in order) over the step table's rows.
+    Sample ids are unique within a step (workload.py:225-236 id_base)."""
+    ids = np.asarray(table["ids"], dtype=np.int64)
+    row = {int(sid): i for i, sid in enumerate(ids.tolist())}
+    S = len(ids)
+    seq = np.full(S, -1, np.int64)
+    off = np.zeros(S, np.int64)
+    span = np.zeros(S, np.int64)
+    fills = []
+    for q, ps in enumerate(sequences):
+        f = 0
+        for k, (sid, tok) in enumerate(ps.spans):
+            i = row[int(sid)]
+            seq[i], off[i], span[i] = q, f, k
+            f += int(tok)
+        fills.append(f)
+    return seq, off, span, fills
+
+
+def _plan_packed(lens, mods, ids, seq, off, span, fills, n_seq, capacity, gbs, dp, sp, world,
+                 mbs, method, pooled):
+    S = len(lens)
     if gbs % (dp * mbs) != 0:
         raise OracleConfigError(
             f"global batch {gbs} not divisible by dp {dp} x microbatch size {mbs}")

@@ -78,7 +78,7 @@ _SIGS = [
     ("mux_segcopy_signal", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, _P, C.c_int32, _P,
                                      _P, _P, _P]),
     ("mux_segcopy_ex", C.c_int, [C.POINTER(PlanCfg), _P, C.c_int32, _P, _P, C.c_int32,
-                                 C.c_int32, _P, _P, _P, _P]),
+                                 C.c_int32, _P, _P, _P, _P, _P]),
     ("mux_copy_bytes", C.c_int, [_P, _P, C.c_int64, C.c_int32, _P]),
     ("mux_memcpy_async", C.c_int, [_P, _P, C.c_int64, _P]),
     ("mux_signal", C.c_int, [C.c_int32, C.c_int32, _P, _P, _P]),
@@ -99,7 +99,7 @@ _SIGS = [
                                            C.c_int32, _P]),
     ("mux_proj_scatter_grouped_signal", C.c_int, [C.POINTER(ProjGroup), C.c_int32, C.c_int32,
                                                   _P, C.c_int32, C.c_int32, C.c_int32, _P, _P,
-                                                  _P, _P, _P, _P]),
+                                                  _P, _P, _P, _P, _P]),
 ]
 EXPORTS = tuple(n for n, _, _ in _SIGS)
 

@@ -17,7 +17,7 @@ step planner uses):
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
@@ -91,6 +91,8 @@ def grouped_reorder(group: ReorderGroup, microbatch_window: int = 1, method: str
     index in group, list position) as the loader would at load time
     (SPEC.md:51).  Within a destination rank, samples are ordered by
     (origin rank, origin position) — the natural all-to-allv receive order.
+    Like the reference's operations, the caller's Samples are not mutated:
+    the returned lists hold copies carrying their origin fields.
     """
     if microbatch_window < 1:
         raise ValueError("microbatch_window must be >= 1")
@@ -100,7 +102,9 @@ def grouped_reorder(group: ReorderGroup, microbatch_window: int = 1, method: str
         shape.append(len(lst))
         for pos, s in enumerate(lst):
             if s.origin_rank < 0:
-                s.origin_rank, s.origin_pos = r, pos
+                s = replace(s, origin_rank=r, origin_pos=pos)
+            else:
+                s = replace(s)
             pool.append(s)
     g = len(group.ranks)
     out: list[list[Sample]] = [[] for _ in range(g)]

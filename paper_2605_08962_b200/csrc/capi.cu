@@ -22,7 +22,7 @@ int cuda_status(cudaError_t e, const char* where) {
 
 }  // namespace mux
 
-extern "C" int mux_version(void) { return 2; }
+extern "C" int mux_version(void) { return 3; }
 
 extern "C" void mux_abi_sizes(int64_t* out) {
   out[0] = (int64_t)sizeof(mux_plan_cfg);

@@ -70,7 +70,14 @@ struct GroupParams {
   // kernels before this one in the stream only read the receive windows)
   uint64_t* const* e_flags_peers;
   uint64_t* e_epoch_ctr;
+  // status word of the path (nullable): nonzero = poisoned step (segcopy.cu):
+  // compute nothing, publish the epoch with kPoisonBit
+  const int32_t* poison;
 };
+
+__device__ __forceinline__ bool is_poisoned(const GroupParams& P) {
+  return P.poison && *(volatile const int32_t*)P.poison != 0;
+}
 
 // E signal by one thread at kernel start (see GroupParams).
 __device__ __forceinline__ void consumed_signal(const GroupParams& P) {
@@ -149,7 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tm.stride[g] = block_stride(tm.num_m[g]);
     tm.tiles[g + 1] = tm.tiles[g] + (int64_t)tm.num_m[g] * num_n;
   }
-  const int64_t num_tiles = tm.tiles[G];
+  const bool poisoned = is_poisoned(P);
+  const int64_t num_tiles = poisoned ? 0 : tm.tiles[G];
 
   if (warp == 0 && lane == 0) {
     if (blockIdx.x == 0) consumed_signal(P);
@@ -317,9 +325,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         *P.epoch_ctr = e;
       }
       __threadfence_system();
+      const uint64_t v = poisoned ? (e | kPoisonBit) : e;
       if (lane < P.world) {
         uint64_t* f = P.flags_peers[lane] + P.me;
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
       }
     }
   }
@@ -375,7 +384,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tm.stride[g] = block_stride(tm.num_m[g]);
     tm.tiles[g + 1] = tm.tiles[g] + (int64_t)tm.num_m[g] * num_n;
   }
-  const int64_t num_tiles = tm.tiles[G];
+  // the poison decision must be the same in both CTAs of a pair (the leader's
+  // MMAs wait for the peer's loads): the leader reads it, the peer copies it
+  __shared__ uint32_t s_poison;
+  if (threadIdx.x == 0 && leader) s_poison = is_poisoned(P) ? 1u : 0u;
 
   if (warp == 0 && lane == 0) {
     if (blockIdx.x == 0) consumed_signal(P);
@@ -398,6 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const bool poisoned = ld_shared_cluster_u32(mapa(smem_u32(&s_poison), 0)) != 0;
+  const int64_t num_tiles = poisoned ? 0 : tm.tiles[G];
 
   if (warp == 0) {
     if (lane == 0) {
@@ -538,9 +552,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         *P.epoch_ctr = e;
       }
       __threadfence_system();
+      const uint64_t v = poisoned ? (e | kPoisonBit) : e;
       if (lane < P.world) {
         uint64_t* f = P.flags_peers[lane] + P.me;
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
       }
     }
   }
@@ -608,7 +623,7 @@ extern "C" int mux_proj_scatter_grouped(const mux_proj_group* groups, int32_t n_
                                         int32_t N, void* const* out_bases, int32_t num_sms,
                                         void* stream) {
   return mux_proj_scatter_grouped_signal(groups, n_groups, N, out_bases, num_sms, 0, 0, nullptr,
-                                         nullptr, nullptr, nullptr, nullptr, stream);
+                                         nullptr, nullptr, nullptr, nullptr, nullptr, stream);
 }
 
 extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int32_t n_groups,
@@ -617,7 +632,8 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
                                                uint64_t* const* flags_peers, uint32_t* sync,
                                                uint64_t* epoch_ctr,
                                                uint64_t* const* e_flags_peers,
-                                               uint64_t* e_epoch_ctr, void* stream) {
+                                               uint64_t* e_epoch_ctr, const int32_t* poison,
+                                               void* stream) {
   using namespace proj;
   if (world > 0 && (!flags_peers || !sync || !epoch_ctr || world > 32 || me < 0 || me >= world)) {
     set_error("projector signal: need flags, sync and epoch pointers, 0 <= me < world <= 32");
@@ -662,6 +678,7 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
   P.world = world;
   P.e_flags_peers = world > 0 ? e_flags_peers : nullptr;
   P.e_epoch_ctr = e_epoch_ctr;
+  P.poison = poison;
   if (P.n_groups == 0) {
     // nothing to compute: still publish the epochs (peers wait for them)
     if (P.e_flags_peers) {

@@ -13,6 +13,12 @@
 //
 // The last CTA to finish fences at system scope and publishes `epoch` into the
 // completion flag of every peer, so the exchange needs no host round trip.
+//
+// Failure path: `poison` (nullable device int32, the path's status word) is
+// set by a flag wait that timed out (1) or that saw a poisoned peer flag (2).
+// A copy launched on a poisoned path moves nothing and publishes its epoch
+// with kPoisonBit set, so every peer's wait fails fast instead of copying
+// over partial data; waits on a poisoned path return at once.
 
 #include <cstdlib>
 
@@ -127,6 +133,7 @@ struct SegArgs {
   int32_t me, world;
   int32_t skip_rank;    // segments addressed to this rank are not copied (-1: none)
   int32_t grab;         // chunks per grab (0: adaptive)
+  const int32_t* poison;  // status word: nonzero = step poisoned, copy nothing
 };
 
 // Work distribution is dynamic: CTAs grab chunks (1 for a local copy, kGrab
@@ -141,8 +148,9 @@ __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int sm
   extern __shared__ int32_t s_c0[];
   __shared__ uint32_t s_grab[2];
   __shared__ bool s_last;
-  const int64_t nchunks = *a.hdr_chunks;
-  const int nseg = (int)*a.hdr_segs;
+  const bool poisoned = a.poison && *(volatile const int32_t*)a.poison != 0;
+  const int64_t nchunks = poisoned ? 0 : *a.hdr_chunks;
+  const int nseg = poisoned ? 0 : (int)*a.hdr_segs;
   const bool staged = nseg < smem_segs;
   if (staged)
     for (int i = threadIdx.x; i <= nseg; i += blockDim.x) s_c0[i] = (int32_t)a.chunk0[i];
@@ -199,9 +207,10 @@ __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int sm
     __syncwarp();
     if (threadIdx.x == 0) *a.epoch_ctr = e;
     __threadfence_system();
+    const uint64_t v = poisoned ? (e | kPoisonBit) : e;
     if (threadIdx.x < a.world) {
       uint64_t* f = a.flags_peers[threadIdx.x] + a.me;
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
     }
   }
 }
@@ -242,11 +251,16 @@ __global__ void wait_kernel(int world, const uint64_t* flags, const uint64_t* ep
                             uint64_t target, int64_t timeout_ns, int32_t* err) {
   const int r = threadIdx.x;
   if (r >= world) return;
+  if (*(volatile int32_t*)err != 0) return;  // poisoned path: fail fast
   const uint64_t epoch = epoch_ctr ? *epoch_ctr : target;
   const uint64_t t0 = global_ns();
   for (;;) {
     uint64_t v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + r) : "memory");
+    if (v & kPoisonBit) {  // the peer's step was poisoned: so is ours
+      atomicCAS(err, 0, 2);
+      break;
+    }
     if (v >= epoch) break;
     if ((int64_t)(global_ns() - t0) > timeout_ns) {
       atomicExch(err, 1);
@@ -402,13 +416,13 @@ extern "C" int mux_segcopy_signal(const mux_plan_cfg* cfg, const void* plan, int
                                   int32_t grid_ctas, uint64_t* const* flags_peers,
                                   uint32_t* sync, uint64_t* epoch_ctr, void* stream) {
   return mux_segcopy_ex(cfg, plan, which, src_bases, dst_bases, grid_ctas, -1, flags_peers, sync,
-                        epoch_ctr, stream);
+                        epoch_ctr, nullptr, stream);
 }
 
 extern "C" int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t which,
                               void* const* src_bases, void* const* dst_bases, int32_t grid_ctas,
                               int32_t skip_rank, uint64_t* const* flags_peers, uint32_t* sync,
-                              uint64_t* epoch_ctr, void* stream) {
+                              uint64_t* epoch_ctr, const int32_t* poison, void* stream) {
   mux_plan_layout L;
   int st = mux_plan_layout_of(cfg, &L);
   if (st) return st;
@@ -443,6 +457,7 @@ extern "C" int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t
   a.me = cfg->me;
   a.world = cfg->world;
   a.skip_rank = skip_rank;
+  a.poison = poison;
   static int grab = -1;  // MUX_COPY_GRAB (tuning; 0 = adaptive)
   if (grab < 0) {
     const char* e = getenv("MUX_COPY_GRAB");

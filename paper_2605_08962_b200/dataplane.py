@@ -161,7 +161,15 @@ class MuxPath:
         self.copy_grid = int(os.environ.get("MUX_COPY_GRID", "0"))
         self.dispatch_grid = int(os.environ.get("MUX_DISPATCH_GRID", str(self.copy_grid)))
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+        # status word of the exchanges (the poison of segcopy.cu): a flag wait
+        # that times out sets 1, one that sees a poisoned peer sets 2; later
+        # copies and GEMMs then move nothing and pass the poison on, later waits
+        # return at once.  run_pipeline mirrors it to the host asynchronously and
+        # raises at its next call once the copy has landed; check_wait() syncs.
         self.wait_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._status_host = torch.zeros(1, dtype=torch.int32).pin_memory() if world > 1 else None
+        self._status_ev = None
+        self.step_done = None  # run_pipeline: the current step's "inputs no longer read" event
         self.recv_dst = _ptr_table([self.recv[g].ptrs[r] for r in range(world)
                                     for g in range(N_GROUPS)], dev)
         self.llm_dst = [_ptr_table(b.ptrs, dev) for b in self.llm_bufs]
@@ -288,9 +296,20 @@ class MuxPath:
         step k's return, as soon as every rank signalled that step k's receive
         windows were consumed.  encoder(k, plan, stream) runs between a step's
         dispatch and its return (the encoder forward); after_step(k, plan,
-        stream) after the return.  kernel_events[k]: (start, end) events around
-        step k's return kernel."""
+        stream) after the return; `self.step_done` is then the event after which
+        step k's plan and inputs are no longer read (with the staged projector
+        it is on the projector stream: wait for it before reusing step k's input
+        buffers).  kernel_events[k]: (start, end) events around step k's return
+        kernel.  Without start_event the call is ordered after everything
+        already enqueued on `stream`.  Raises RuntimeError when an earlier call
+        left the path poisoned (a timed-out flag wait; see check_wait)."""
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.poll_status()
+        if start_event is None:
+            # order this call after everything already on `main` (inputs written
+            # there, and an earlier call's encoder still reading the windows)
+            start_event = _event()
+            start_event.record(main)
         if steps is not None:
             n = len(steps)
             fixed = {k: (steps[k][0], steps[k][1], None) for k in range(n)}
@@ -349,9 +368,16 @@ class MuxPath:
                 cs.wait_event(self._ready[slot[k + 1]])
                 self.dispatch_overlapped(self._ring[slot[k + 1]], get(k + 1)[1], cs, after=ev)
                 self._dispatched[slot[k + 1]].record(cs)
+            self.step_done = self._freed[s]
             if after_step is not None:
                 after_step(k, p, main)
+            if steps is None:  # streaming: step k's inputs are issued; drop them
+                cache.pop(k, None)
         self._kstep = base + n
+        if self._status_host is not None:  # async status mirror, raised at the next call
+            self._status_host.copy_(self.wait_err, non_blocking=True)
+            self._status_ev = _event()
+            self._status_ev.record(main)
 
     def _arena_table(self, arenas) -> torch.Tensor:
         """Device table of loader-arena pointers, cached per arena set (no sync
@@ -388,7 +414,7 @@ class MuxPath:
         _lib.check(L.mux_segcopy_ex(C.byref(plan.cfg), plan.ptr, which, src.data_ptr(),
                                     dst.data_ptr(), grid, -1, fptrs.data_ptr(),
                                     self.sync[2 * which:].data_ptr(), epoch.data_ptr(),
-                                    s), "mux_segcopy_ex")
+                                    self.wait_err.data_ptr(), s), "mux_segcopy_ex")
         if ke is not None:
             ke[1].record(stream if stream is not None else torch.cuda.current_stream(self.device))
         _lib.check(L.mux_wait(self.world, flags.tensor.data_ptr(), epoch.data_ptr(),
@@ -505,7 +531,8 @@ class MuxPath:
                 self.rank,
                 self.world, self.flag_ptrs.data_ptr(), self.sync[6:].data_ptr(),
                 self.epoch_ctr.data_ptr(), self.flag_ptrs_e.data_ptr() if fe else None,
-                self.epoch_e.data_ptr() if fe else None, s), "mux_proj_scatter_grouped_signal")
+                self.epoch_e.data_ptr() if fe else None, self.wait_err.data_ptr(), s),
+                "mux_proj_scatter_grouped_signal")
         if ke is not None:
             ke[1].record(main)
         if self.world > 1:
@@ -635,9 +662,29 @@ class MuxPath:
         graph node, so the host issues one launch per step."""
         return StepGraphs(self, dtabs, arenas_list)
 
+    _POISON_WHY = {1: "a cross-GPU completion flag wait timed out",
+                   2: "a peer rank's step was poisoned (its flag wait timed out)"}
+
+    def _raise_status(self, code: int):
+        raise RuntimeError(f"data path poisoned: {self._POISON_WHY.get(code, code)}; the "
+                           "exchange buffers of this and later steps are not valid (rebuild "
+                           "the MuxPath)")
+
     def check_wait(self):
-        if int(self.wait_err.item()):
-            raise RuntimeError("cross-GPU completion flag wait timed out")
+        """Synchronise and raise if the path is poisoned."""
+        code = int(self.wait_err.item())
+        if code:
+            self._raise_status(code)
+
+    def poll_status(self):
+        """Raise if an earlier run_pipeline's status copy has landed and shows a
+        poisoned path (no synchronisation)."""
+        ev = self._status_ev
+        if ev is not None and ev.query():
+            self._status_ev = None
+            code = int(self._status_host[0])
+            if code:
+                self._raise_status(code)
 
 
 class StepGraphs:

@@ -30,13 +30,34 @@ def test_exchange_summary():
     assert x["return_remote_frac"] == pytest.approx(1900 / 7000)
 
 
-def test_measured_traffic_scales_the_captured_ratio():
+def test_captured_traffic_reports_the_capture():
     rec = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
     for name in ("cfg2", "target1"):
         r = rec[name]
-        ratio = (r["dram_read"] + r["dram_write"]) / r["algorithmic_bytes"]
-        assert 0.5 < ratio < 1.2  # reads equal the algorithmic bytes; writes partly in L2
-        t, src = bench.measured_traffic(name, 1e9)
-        assert t == pytest.approx(1e9 * ratio) and "ncu" in src
-    t, src = bench.measured_traffic("no_such_config", 1e9)
+        t, src = bench.captured_traffic(name)
+        assert t == r["dram_read"] + r["dram_write"] and "ncu" in src
+        assert 0.5 < t / r["algorithmic_bytes"] < 1.2  # no wasted re-reads
+    t, src = bench.captured_traffic("no_such_config")
     assert t is None and "no ncu capture" in src
+
+
+def test_tensor_peak_follows_the_clock_record():
+    _, burst, sus, _ = bench.peaks()
+    full = {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": []}
+    assert bench.choose_tensor_peak(full)[0] == burst
+    capped = dict(full, reasons=["sw_power_cap"])
+    assert bench.choose_tensor_peak(capped)[0] == sus
+    slow = dict(full, sm_mhz=1300.0)
+    assert bench.choose_tensor_peak(slow)[0] == sus
+
+
+def test_both_arms_print_the_same_config():
+    """The reference arm and ours time the same distinct steps in the same order
+    and print the same `config` dict (the driver compares them)."""
+    class A:
+        steps, warmup, distinct = 20, 5, 8
+    n = bench.n_distinct_of(A)
+    assert n == 8 and bench.timed_indices(A, n)[:4] == [5, 6, 7, 0]
+    a = bench.config_dict("cfg2", 1, n, 43355.0, 55499.25)
+    b = bench.config_dict("cfg2", 1, n, 43355.0, 55499.25)
+    assert a == b and a["workload"] == "cfg2" and a["global_batch"] == 4

@@ -189,7 +189,11 @@ def test_grouped_reorder_and_restore(cuda_device):
               for j in range(int(rs.randint(0, 9)))] for r in range(4)]
     lists[0] += [W.Sample(999 + j, W.Modality.VIDEO, "x", 16000) for j in range(4)]  # skewed rank
     pre = [sum(s.length for s in lst) for lst in lists]
+    before = [[(s.origin_rank, s.origin_pos) for s in lst] for lst in lists]
     out, rec = balance.grouped_reorder(balance.ReorderGroup([0, 1, 2, 3], lists), 2, "kk")
+    # the caller's Samples are not mutated (reference ops return new objects)
+    assert [[(s.origin_rank, s.origin_pos) for s in lst] for lst in lists] == before
+    assert all(s.origin_rank >= 0 for lst in out for s in lst)
     post = [sum(s.length for s in lst) for lst in out]
     assert balance.imbalance(post) < balance.imbalance(pre)
     back = balance.restore_order(rec, out)

@@ -105,7 +105,7 @@ def test_capi_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(L, name), name
     assert declared == set(_lib.EXPORTS)
-    assert L.mux_version() == 2
+    assert L.mux_version() == 3
 
 
 def test_plan_layout_on_cpu():

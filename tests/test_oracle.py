@@ -108,6 +108,57 @@ def test_kk_bounds_random():
             assert abs(loads.sum() - sum(w)) < 1e-6
 
 
+def _opt_max_load(w, g):
+    """Exhaustive optimum of the g-way max load (branch and bound, heaviest first)."""
+    w = sorted(w, reverse=True)
+    best = [sum(w)]
+    loads = [0.0] * g
+
+    def rec(k):
+        if k == len(w):
+            best[0] = min(best[0], max(loads))
+            return
+        seen = set()
+        for r in range(g):
+            if loads[r] in seen or loads[r] + w[k] >= best[0]:
+                continue
+            seen.add(loads[r])
+            loads[r] += w[k]
+            rec(k + 1)
+            loads[r] -= w[k]
+
+    rec(0)
+    return best[0]
+
+
+def test_kk_within_four_thirds_of_optimum():
+    """n <= 12, g <= 4 -> KK max load <= 4/3 x the exhaustive optimum."""
+    rs = np.random.RandomState(11)
+    worst = 0.0
+    for _ in range(150):
+        g = int(rs.randint(1, 5))
+        n = int(rs.randint(1, 13))
+        w = rs.lognormal(5, 0.8, size=n).round().clip(1).tolist()
+        kk = np.bincount(oplan.kk_assign(w, g), weights=w, minlength=g).max()
+        opt = _opt_max_load(w, g)
+        assert kk <= 4.0 / 3.0 * opt + 1e-9, (w, g, kk, opt)
+        worst = max(worst, kk / opt)
+    assert worst >= 1.0
+
+
+def test_kk_beats_round_robin_on_lognormal_instances():
+    """over 1000 seeded lognormal instances (n=64, g=8), KK's
+    max/mean imbalance <= round-robin-by-arrival's in >= 95% of them."""
+    rs = np.random.RandomState(2605)
+    wins = 0
+    for _ in range(1000):
+        w = rs.lognormal(6, 1.0, size=64).round().clip(1).tolist()
+        kk = np.bincount(oplan.kk_assign(w, 8), weights=w, minlength=8)
+        rr = np.bincount(np.arange(64) % 8, weights=w, minlength=8)
+        wins += kk.max() / kk.mean() <= rr.max() / rr.mean() + 1e-12
+    assert wins >= 950, wins
+
+
 def test_reorder_indivisible_floor():
     # SPEC.md:405: 4 ranks holding [10,1,1,1] -> max load stays 10, imbalance 10/3.25
     r = oplan.lpt_assign([10.0, 1.0, 1.0, 1.0], [0, 1, 2, 3], 4)
