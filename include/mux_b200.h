@@ -124,7 +124,25 @@ typedef struct {
    * mux_text_embed can gather the text tokens' embedding rows into the same
    * packed LLM buffer. */
   int32_t text_embed;
+  /* Reorder groups (SPEC.md:383 ReorderGroup, :208 reorder_group_size):
+   * consecutive blocks of reorder_group ranks; a sample is balanced only over
+   * the ranks of its origin rank's group (0 = the whole world). */
+  int32_t reorder_group;
+  /* Per-sample balancing cost (SPEC.md:390 token counts by default; the
+   * optional encoder cost of costs.flops_forward, costs.py:108-124):
+   * MUX_COST_TOKENS: cost = len;  MUX_COST_FLOPS: cost = cost_lin[g] * len +
+   * cost_quad[g] * len * len for encoder group g, i.e. flops_forward with
+   * cost_lin = 2 P, cost_quad = 2 layers hidden (encoder seq_len = len), mult 1.
+   * Integer-valued parameters keep every cost and load sum exact in fp64
+   * (bit-identical plans on every rank) while the sums stay below 2^50. */
+  int32_t cost_model;
+  int32_t reserved0;
+  double cost_lin[MUX_N_GROUPS];
+  double cost_quad[MUX_N_GROUPS];
 } mux_plan_cfg;
+
+#define MUX_COST_TOKENS 0
+#define MUX_COST_FLOPS 1
 
 #define MUX_RESHARD_ULYSSES 0
 #define MUX_RESHARD_CP_HYBRID 1
@@ -335,7 +353,7 @@ typedef struct {
   int64_t M_max;           /* rows X can hold; 0 drops the group               */
   const int64_t* M_dev;    /* device row count (clamped to M_max) or NULL      */
   int32_t K, reserved;
-  const int64_t* row_dst;  /* int64 [M_max]: (rank << 40) | row                */
+  const int64_t* row_dst;  /* int64 [M_max]: (rank << 40) | row; NULL = row m of out_bases[0] */
 } mux_proj_group;
 
 /* Every group's projector + scatter in ONE persistent launch (tiles of group
@@ -356,6 +374,24 @@ int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int32_t n_grou
                                     int32_t world, uint64_t* const* flags_peers, uint32_t* sync,
                                     uint64_t* epoch_ctr, uint64_t* const* e_flags_peers,
                                     uint64_t* e_epoch_ctr, const int32_t* poison, void* stream);
+
+/* Backward of the projector (no reference kernel; the gradient path of
+ * SPEC.md:411 and PAPER.md:1114), on the encoder rank after the gradient
+ * return: G bf16 [M_max, N] = dL/dY of the encoder rows in encoder order,
+ * X bf16 [M_max, K] = the projector input, W bf16 [N, K] the weight.
+ *   dX bf16 [M_max, K] = G . W        (rows < M written)
+ *   dW bf16 [N, K]     = G^T . X      (fp32 accumulation, deterministic)
+ *   db bf16 [N]        = sum_m G[m,:] (fused into the dW launch; NULL = skip)
+ * M = *M_dev clamped to M_max (M_dev NULL: M_max).  dX or dW may be NULL to
+ * skip that product.  Rows [M, round_up(M, 64)) of G and X are zeroed.
+ * tcgen05 CTA-pair GEMMs (MN-major operands for dW); K % 256 == 0,
+ * N % 256 == 0.  workspace >= mux_proj_backward_workspace(K, N, num_sms)
+ * bytes (W^T, split-K partials); num_sms = SMs the launches may use (0: all). */
+size_t mux_proj_backward_workspace(int32_t K, int32_t N, int32_t num_sms);
+int mux_proj_backward(const uint16_t* G, const uint16_t* X, const uint16_t* W, int64_t M_max,
+                      const int64_t* M_dev, int32_t K, int32_t N, uint16_t* dX, uint16_t* dW,
+                      uint16_t* db, void* workspace, size_t workspace_bytes, int32_t num_sms,
+                      void* stream);
 
 #ifdef __cplusplus
 }

@@ -136,13 +136,18 @@ def ulysses_split(fill, sp):
 # ----------------------------------------------------------------------------
 
 def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=False,
-              packed=None):
+              packed=None, reorder_group=0, cost=None):
     """Plan one step.  `table` dict: lens, mods, ids (arrays over S samples),
     carry_seq (array over the first n_carry samples: their carry sequence),
     n_carry_seqs, chunk_off (offsets of drawn chunks, first = n_carry).
     packed: optional (seq, off, span, fills) of an FFD placement computed
     elsewhere — bench.py's reference arm passes the reference's own
-    hybrid_pack output (packed_from_sequences) and times only the rest here."""
+    hybrid_pack output (packed_from_sequences) and times only the rest here.
+    reorder_group: ranks per reorder group (0 = world): a sample is
+    balanced over the ranks of its origin's group only.  cost: None (token
+    counts, SPEC.md:390) or per-encoder-group (lin, quad) pairs, cost =
+    lin * L + quad * L * L — costs.flops_forward (costs.py:108-124) with
+    lin = 2 P, quad = 2 layers hidden, mult 1."""
     lens = np.asarray(table["lens"], dtype=np.int64)
     mods = np.asarray(table["mods"], dtype=np.int64)
     ids = np.asarray(table["ids"], dtype=np.int64)
@@ -168,7 +173,7 @@ def plan_step(table, capacity, gbs, dp, sp, world, mbs=1, method="lpt", pooled=F
         seq, off, span, fills, n_seq = _ffd_table(lens, ids, carry_seq, n_carry_seqs, chunk_off,
                                                   capacity)
     return _plan_packed(lens, mods, ids, seq, off, span, fills, n_seq, capacity, gbs, dp, sp,
-                        world, mbs, method, pooled)
+                        world, mbs, method, pooled, reorder_group, cost)
 
 
 def _ffd_table(lens, ids, carry_seq, n_carry_seqs, chunk_off, capacity):
@@ -228,8 +233,16 @@ def packed_from_sequences(table, sequences):
     return seq, off, span, fills
 
 
+def sample_cost(L, group, cost):
+    """Balancing cost of one sample (exact in fp64 for integer parameters)."""
+    if cost is None:
+        return float(L)
+    lin, quad = cost[group]
+    return float(lin) * float(L) + float(quad) * float(L) * float(L)
+
+
 def _plan_packed(lens, mods, ids, seq, off, span, fills, n_seq, capacity, gbs, dp, sp, world,
-                 mbs, method, pooled):
+                 mbs, method, pooled, reorder_group=0, cost=None):
     S = len(lens)
     if gbs % (dp * mbs) != 0:
         raise OracleConfigError(
@@ -284,26 +297,32 @@ def _plan_packed(lens, mods, ids, seq, off, span, fills, n_seq, capacity, gbs, d
         arena_rows[origin[i], group[i]] += lens[i]
 
     enc = np.full(S, -1, np.int64)
-    pools = [enc_item] if pooled else [[i for i in enc_item if group[i] == q]
-                                       for q in range(N_GROUPS)]
-    for items in pools:
+    RG = reorder_group or world
+    if world % RG:
+        raise ValueError(f"reorder group {RG} must divide world {world}")
+    pools = []  # (reorder group, encoder group or pooled), table order inside
+    for rg in range(world // RG):
+        mine = [i for i in enc_item if origin[i] // RG == rg]
+        pools += [(rg, mine)] if pooled else [(rg, [i for i in mine if group[i] == q])
+                                              for q in range(N_GROUPS)]
+    for rg, items in pools:
         if not items:
             continue
-        costs = [float(lens[i]) for i in items]
-        if world == 1:
+        costs = [sample_cost(lens[i], group[i], cost) for i in items]
+        if RG == 1:
             ranks = [0] * len(items)
         elif method == "lpt":
-            ranks = lpt_assign(costs, [int(ids[i]) for i in items], world)
+            ranks = lpt_assign(costs, [int(ids[i]) for i in items], RG)
         elif method == "kk":
-            ranks = kk_assign(costs, world)
+            ranks = kk_assign(costs, RG)
         elif method in ("lpt_local", "lpt_local_rw"):
             ranks = lpt_local_assign(costs, [int(ids[i]) for i in items],
-                                     [int(origin[i]) for i in items], world,
+                                     [int(origin[i]) - rg * RG for i in items], RG,
                                      remote_weight=method == "lpt_local_rw")
         else:
             raise ValueError(f"unknown method {method!r}")
         for i, r in zip(items, ranks):
-            enc[i] = r
+            enc[i] = rg * RG + r
 
     enc_off = np.full(S, -1, np.int64)
     recv_rows = np.zeros((world, N_GROUPS), np.int64)

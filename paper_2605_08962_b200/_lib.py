@@ -35,7 +35,9 @@ class PlanCfg(C.Structure):
         ("chunk_bytes", C.c_int32), ("ret_mode", C.c_int32),
         ("row_bytes_grad", C.c_int32 * N_GROUPS), ("lssp_sp", C.c_int32),
         ("lssp_eta", C.c_int32), ("reshard", C.c_int32), ("cp_threshold", C.c_int32),
-        ("text_embed", C.c_int32)]
+        ("text_embed", C.c_int32), ("reorder_group", C.c_int32), ("cost_model", C.c_int32),
+        ("reserved0", C.c_int32), ("cost_lin", C.c_double * N_GROUPS),
+        ("cost_quad", C.c_double * N_GROUPS)]
 
 
 LAYOUT_FIELDS = (
@@ -49,6 +51,7 @@ LAYOUT_FIELDS = (
     "lp_n", "lp_k", "lp_t0", "lp_len", "lp_row", "text_off", "tseg_src", "tseg_dst",
     "tseg_rows", "tseg_row0", "total")
 RESHARD = {"ulysses": 0, "cp_hybrid": 1}
+COST_TOKENS, COST_FLOPS = 0, 1
 LSSP_MAX = 8
 
 
@@ -100,6 +103,9 @@ _SIGS = [
     ("mux_proj_scatter_grouped_signal", C.c_int, [C.POINTER(ProjGroup), C.c_int32, C.c_int32,
                                                   _P, C.c_int32, C.c_int32, C.c_int32, _P, _P,
                                                   _P, _P, _P, _P, _P]),
+    ("mux_proj_backward_workspace", C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
+    ("mux_proj_backward", C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P, _P,
+                                    _P, C.c_size_t, C.c_int32, _P]),
 ]
 EXPORTS = tuple(n for n, _, _ in _SIGS)
 

@@ -35,6 +35,12 @@ D_IN = (588, 512)      # vision patch row, audio mel-stack row
 D_ENC = (1280, 1280)   # ViT-600M-shaped / audio encoder hidden
 D_LLM = 4096           # 7B-shaped LLM hidden
 
+# Encoder shapes per group for the optional flops-weighted rebalance
+# (costs.flops_forward, pkg/src/muxsim/costs.py:108-124): (params, layers,
+# hidden).  ViT-600M-shaped: 32 layers x 1280 hidden (12 h^2 per layer); the
+# audio encoder is given the same shape (builder's choice).
+ENCODER_SHAPES = ((32 * 12 * 1280 * 1280, 32, 1280), (32 * 12 * 1280 * 1280, 32, 1280))
+
 _CFG5_PHASES = (
     {"openimages": 0.13, "video": 0.0, "librispeech": 0.74, "text": 0.13},
     {"openimages": 0.55, "video": 0.10, "librispeech": 0.0, "text": 0.35},

@@ -103,6 +103,17 @@ def flops_forward(spec: ModelSpec, tokens: int, seq_len: int) -> float:
     return (dense + attention) * spec.flops_multiplier
 
 
+def encoder_cost_params(spec: ModelSpec) -> tuple[float, float]:
+    """(lin, quad) of the device planner's flops cost model (mux_plan_cfg
+    cost_model = MUX_COST_FLOPS): lin L + quad L^2 == flops_forward(spec, L, L)
+    bit for bit (an encoder's seq_len is the sample length, costs.py:112-114),
+    which needs integer-valued params/layers/hidden and multiplier 1 so that
+    every cost and load sum stays an exact fp64 integer on every rank."""
+    if spec.flops_multiplier != 1.0 or float(spec.params) != int(spec.params):
+        raise ValueError("the device cost model needs integer params and flops_multiplier 1")
+    return 2.0 * spec.params, 2.0 * spec.layers * spec.hidden
+
+
 def flops_backward(spec: ModelSpec, tokens: int, seq_len: int) -> float:
     return 2.0 * flops_forward(spec, tokens, seq_len)
 

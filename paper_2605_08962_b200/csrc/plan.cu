@@ -68,6 +68,19 @@ static int compute_layout(const mux_plan_cfg& c, mux_plan_layout* L) {
                 c.lssp_sp, MUX_LSSP_MAX, c.world);
       return MUX_ERR_VALUE;
     }
+    const int rg = c.reorder_group > 0 ? c.reorder_group : c.world;
+    if (c.reorder_group < 0 || c.world % rg || (c.lssp_sp > 0 && rg % c.lssp_sp)) {
+      set_error("reorder group %d: need 0 (world) or a divisor of world %d that LSSP groups "
+                "(%d) divide", c.reorder_group, c.world, c.lssp_sp);
+      return MUX_ERR_VALUE;
+    }
+    if (c.cost_model != MUX_COST_TOKENS &&
+        (c.cost_model != MUX_COST_FLOPS || !(c.cost_lin[0] >= 0) || !(c.cost_lin[1] >= 0) ||
+         !(c.cost_quad[0] >= 0) || !(c.cost_quad[1] >= 0))) {
+      set_error("cost model %d: need tokens (0) or flops (1) with non-negative parameters",
+                c.cost_model);
+      return MUX_ERR_VALUE;
+    }
     if (c.reshard != MUX_RESHARD_ULYSSES &&
         (c.reshard != MUX_RESHARD_CP_HYBRID || c.ret_mode != MUX_RET_FINAL ||
          c.cp_threshold < 0 || c.sp > 8)) {
@@ -726,7 +739,7 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
   __shared__ int64_t s_wk[32 * kMaxKeys];
   __shared__ int64_t s_carry[kMaxKeys];
   __shared__ int32_t s_chbase[kMaxChunks + 1];
-  __shared__ int32_t s_misc[4];
+  __shared__ int32_t s_misc[8 + kMaxKeys + 1];  // scalars, then the pool offsets of G
   const int tid = threadIdx.x, nt = blockDim.x;
   const int S = cfg.S, nc = cfg.n_carry, nch = cfg.n_chunks, W = cfg.world;
   const int max_seq = cfg.n_carry_seqs + (S - nc) + 1;
@@ -946,9 +959,13 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
   for (int x = tid; x < W * MUX_N_GROUPS; x += nt) p.arena_rows[x] = s_carry[x];
 
   // ---- G. encoder assignment: one sort over (pool, -cost, id, index), then
-  //         one warp per pool (LPT), or KK pool by pool --------------------------
+  //         one warp per pool (LPT), or KK pool by pool.  A pool = (reorder
+  //         group of the origin rank, encoder group unless pooled); each pool
+  //         is balanced over the RG ranks of its reorder group ----------------
   stamp(p, 22);
-  const int npools = cfg.pooled ? 1 : MUX_N_GROUPS;
+  const int ngrp = cfg.pooled ? 1 : MUX_N_GROUPS;
+  const int RG = cfg.reorder_group > 0 ? cfg.reorder_group : W;
+  const int npools = (W / RG) * ngrp;  // <= 8 * 2 = kMaxKeys
   const int spad = next_pow2(S > 0 ? S : 1);
   double* l_cost = reinterpret_cast<double*>(smem + SL.lpt);
   int64_t* l_id = reinterpret_cast<int64_t*>(l_cost + spad);
@@ -958,63 +975,80 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
   int32_t* l_rank = l_ord + spad;
   int32_t* l_org = l_rank + spad;
   int32_t* l_flag = l_org + spad;
+  int* s_poff = s_misc + 8;  // pool offsets [npools + 1] (s_misc holds 8 + kMaxKeys + 1)
+  auto pool_of = [&](int i) {
+    return (w.org[i] / RG) * ngrp + (cfg.pooled ? 0 : w.grp[i]);
+  };
   if (tid < kMaxKeys) s_carry[tid] = 0;
   __syncthreads();
   for (int base = 0; base < S; base += nt) {  // position of each encoder item in its pool
     const int i = base + tid;
     const bool e = i < S && enc_item(i);
-    const int pool = e ? (cfg.pooled ? 0 : w.grp[i]) : -1;
+    const int pool = e ? pool_of(i) : -1;
     const int64_t pre = multi_scan(pool, 1, npools, s_wk, s_carry);
     if (e) w.within[i] = (int32_t)pre;
   }
   if (tid == 0) {
-    s_misc[2] = (int)s_carry[0];
-    s_misc[3] = npools > 1 ? (int)s_carry[1] : 0;
+    int acc = 0;
+    for (int q = 0; q < npools; ++q) {
+      s_poff[q] = acc;
+      acc += (int)s_carry[q];
+    }
+    s_poff[npools] = acc;
   }
   __syncthreads();
-  const int m0 = s_misc[2], m1 = s_misc[3], m = m0 + m1;
-  for (int i = tid; i < S; i += nt) {  // pool-major item order
-    if (enc_item(i)) {
-      const int pool = cfg.pooled ? 0 : w.grp[i];
-      w.order[(pool == 0 ? 0 : m0) + w.within[i]] = i;
-    }
-  }
+  const int m = s_poff[npools];
+  for (int i = tid; i < S; i += nt)  // pool-major item order
+    if (enc_item(i)) w.order[s_poff[pool_of(i)] + w.within[i]] = i;
   __syncthreads();
   for (int v = tid; v < spad; v += nt) {
     if (v < m) {
       const int i = w.order[v];
-      l_cost[v] = (double)w.len[i];
+      const int q = pool_of(i);
+      const double L = (double)w.len[i];
+      const int g = w.grp[i];
+      // exact in fp64: integer-valued parameters (mux_plan_cfg.cost_model)
+      l_cost[v] = cfg.cost_model == MUX_COST_FLOPS
+                      ? __dadd_rn(__dmul_rn(cfg.cost_lin[g], L),
+                                  __dmul_rn(__dmul_rn(cfg.cost_quad[g], L), L))
+                      : L;
       l_id[v] = w.id[i];
       l_tidx[v] = i;
-      l_pool[v] = v < m0 ? 0 : 1;
-      l_org[v] = w.org[i];
+      l_pool[v] = q;
+      l_org[v] = w.org[i] - (w.org[i] / RG) * RG;  // origin within its reorder group
     }
     l_ord[v] = v;
   }
   __syncthreads();
+  bool kk_overflow = false;
   if (m > 0) {
-    if (W == 1) {
+    if (RG == 1) {
       for (int v = tid; v < m; v += nt) l_rank[v] = 0;
     } else if (cfg.method == MUX_LPT || cfg.method == MUX_LPT_LOCAL ||
                cfg.method == MUX_LPT_LOCAL_RW) {
       bitonic_sort(l_ord, next_pow2(m), PoolKey{l_pool, l_cost, l_id, l_tidx, m});
-      const int warp = tid >> 5;
-      if (cfg.method == MUX_LPT) {
-        if (warp == 0 && m0 > 0) lpt_warp(l_ord, l_cost, m0, W, l_rank);
-        if (warp == 1 && m1 > 0) lpt_warp(l_ord + m0, l_cost, m1, W, l_rank);
-      } else {
-        const bool rw = cfg.method == MUX_LPT_LOCAL_RW;
-        if (warp == 0 && m0 > 0) lpt_local_warp(l_ord, l_cost, l_org, m0, W, l_rank, l_flag, rw);
-        if (warp == 1 && m1 > 0)
-          lpt_local_warp(l_ord + m0, l_cost, l_org, m1, W, l_rank, l_flag + m0, rw);
+      const int warp = tid >> 5, nw = nt >> 5;
+      for (int q = warp; q < npools; q += nw) {
+        const int o = s_poff[q], n = s_poff[q + 1] - o;
+        if (n == 0) continue;
+        if (cfg.method == MUX_LPT)
+          lpt_warp(l_ord + o, l_cost, n, RG, l_rank);
+        else
+          lpt_local_warp(l_ord + o, l_cost, l_org, n, RG, l_rank, l_flag + o,
+                         cfg.method == MUX_LPT_LOCAL_RW);
       }
-    } else if (m0 > kKkMax || m1 > kKkMax) {
-      if (tid == 0) p.hdr[MUX_H_ERR_INDEX] = -2;  // KK pool limit
     } else {
-      KkSmem& K = *reinterpret_cast<KkSmem*>(smem + SL.kk);
-      if (tid < 32 && m0 > 0) kk_warp(K, l_cost, m0, W, l_rank);
-      __syncthreads();
-      if (tid < 32 && m1 > 0) kk_warp(K, l_cost + m0, m1, W, l_rank + m0);
+      for (int q = 0; q < npools; ++q) kk_overflow |= s_poff[q + 1] - s_poff[q] > kKkMax;
+      if (kk_overflow) {
+        if (tid == 0) p.hdr[MUX_H_ERR_INDEX] = -2;  // KK pool limit
+      } else {
+        KkSmem& K = *reinterpret_cast<KkSmem*>(smem + SL.kk);
+        for (int q = 0; q < npools; ++q) {
+          const int o = s_poff[q], n = s_poff[q + 1] - o;
+          if (tid < 32 && n > 0) kk_warp(K, l_cost + o, n, RG, l_rank + o);
+          __syncthreads();
+        }
+      }
     }
   }
   __syncthreads();
@@ -1024,6 +1058,9 @@ __device__ void finalize(const mux_plan_cfg& cfg, const int32_t* lens, const int
     set_status(p, MUX_ERR_VALUE);
     return;
   }
+  for (int v = tid; v < m; v += nt)  // rank within the group -> world rank
+    l_rank[v] += (l_pool[v] / ngrp) * RG;
+  __syncthreads();
   for (int v = tid; v < m; v += nt) w.enc[l_tidx[v]] = l_rank[v];
   __syncthreads();
 

@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t m = (int64_t)m_blk * BM + quarter * 32 + lane;
       char* my_dst = nullptr;
       if (m < tm.M[g]) {
-        const int64_t rd = P.row_dst[g][m];
+        const int64_t rd = P.row_dst[g] ? P.row_dst[g][m] : m;  // NULL: row m of base 0
         my_dst = static_cast<char*>(P.out_bases[rd >> 40]) +
                  ((rd & kRowMask) * N + (int64_t)n_blk * BN + colgrp * 128) * 2;
       }
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t m = (int64_t)m_blk * BM2 + (int)rank * 128 + quarter * 32 + lane;
       char* my_dst = nullptr;
       if (m < tm.M[g]) {
-        const int64_t rd = P.row_dst[g][m];
+        const int64_t rd = P.row_dst[g] ? P.row_dst[g][m] : m;  // NULL: row m of base 0
         my_dst = static_cast<char*>(P.out_bases[rd >> 40]) +
                  ((rd & kRowMask) * N + (int64_t)n_blk * BN + colgrp * 128) * 2;
       }

@@ -88,6 +88,21 @@ __device__ __forceinline__ uint64_t sdesc_sw128(const void* smem) {
   const uint64_t a = (smem_u32(smem) >> 4) & 0x3FFF;
   return a | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
+// Shared-memory matrix descriptor, MN-major, 128-byte swizzle (the layout a
+// TMA box of 64 MN-contiguous bf16 x 64 K-rows writes): 8 K-rows x 128 B atoms
+// stacked along K at SBO = 1024 B; the next 64-element MN block at LBO bytes.
+// One K16 step = 16 K-rows = +2048 B (+128 in the encoded start address).
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(const void* smem, uint32_t lbo_bytes) {
+  const uint64_t a = (smem_u32(smem) >> 4) & 0x3FFF;
+  return a | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+// Instruction descriptor kind::f16: D f32, A/B bf16, A/B MN-major when set
+// (bits 15 / 16).
+__host__ __device__ constexpr uint32_t idesc_bf16_f32_major(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 // Instruction descriptor kind::f16: D f32, A/B bf16, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
@@ -200,16 +215,17 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
-// Arrive on an mbarrier of another CTA of the cluster (default semantics, as
-// CUTLASS's ClusterBarrier::arrive).  The pair GEMM's epilogue only needs its
-// TMEM reads ordered before the leader's next MMA, which tcgen05.wait::ld +
-// tcgen05.fence::before_thread_sync provide; a release.cluster arrive made
-// every epilogue warp wait for its global stores (MEMBAR + ERRBAR per tile).
+// 32-bit load from the shared memory of a CTA of the cluster (mapa address)
 __device__ __forceinline__ uint32_t ld_shared_cluster_u32(uint32_t cluster_addr) {
   uint32_t v;
   asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(cluster_addr) : "memory");
   return v;
 }
+// Arrive on an mbarrier of another CTA of the cluster (default semantics, as
+// CUTLASS's ClusterBarrier::arrive).  The pair GEMM's epilogue only needs its
+// TMEM reads ordered before the leader's next MMA, which tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync provide; a release.cluster arrive made
+// every epilogue warp wait for its global stores (MEMBAR + ERRBAR per tile).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }

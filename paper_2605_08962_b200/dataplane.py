@@ -90,7 +90,11 @@ class MuxPath:
                         or "cp_hybrid" (cp_threshold, 0 = capacity / sp);
       text_embed        also emit text segments for `embed_text`;
       overlap_dispatch  `run_pipeline` dispatches step k+1 under step k's
-                        return (E/D/R flag channels, alternating LLM buffers).
+                        return (E/D/R flag channels, alternating LLM buffers);
+      reorder_group     balance each sample only over the ranks of its origin's
+                        group of consecutive ranks (SPEC.md:383; 0 = world);
+      cost              None (token counts) or per-group (lin, quad) flops
+                        weights (costs.encoder_cost_params).
     """
 
     def __init__(self, *, capacity: int, gbs: int, dp: int, sp: int = 1, world: int = 1,
@@ -100,8 +104,11 @@ class MuxPath:
                  wait_timeout_ms: int = 20000, projector_return: str | None = None,
                  lssp_eta: int | None = None, lssp_sp: int = 1, reshard: str = "ulysses",
                  cp_threshold: int = 0, text_embed: bool = False,
-                 overlap_dispatch: bool = False):
+                 overlap_dispatch: bool = False, reorder_group: int = 0, cost=None):
         self.capacity, self.gbs, self.dp, self.sp = capacity, gbs, dp, sp
+        # balancing scope and cost (planner.make_cfg): reorder groups of
+        # consecutive ranks (0 = world) and token or flops costs
+        self.reorder_group, self.cost = reorder_group, cost
         self.world, self.rank, self.method, self.pooled = world, rank, method, pooled
         self.d_in, self.d_enc, self.d_llm = tuple(d_in), tuple(d_enc), d_llm
         self.projector = projector
@@ -217,7 +224,8 @@ class MuxPath:
                         lssp_sp=self.lssp_sp if self.lssp_eta is not None else 0,
                         lssp_eta=self.lssp_eta or 0, reshard=self.reshard,
                         cp_threshold=self.cp_threshold, text_embed=self.text_embed,
-                        chunk_bytes=self.chunk_bytes)
+                        chunk_bytes=self.chunk_bytes, reorder_group=self.reorder_group,
+                        cost=self.cost)
 
     @property
     def llm(self) -> _Window:
@@ -629,16 +637,49 @@ class MuxPath:
             self._dy_tables[key] = t
         self._exchange(plan, 2, t, self.grad_dst, stream)
 
-    def projector_backward(self, group: int, rows: int, x: torch.Tensor | None = None):
-        """dX = dY W and dW = dY^T X for encoder group `group` on this encoder rank,
-        from the returned gradient rows (plain GEMMs: cuBLAS through torch).
-        x: the projector inputs [rows, d_enc] (default: this rank's encoder output)."""
+    def projector_backward(self, group: int, rows: int | None = None,
+                           x: torch.Tensor | None = None, plan: Plan | None = None,
+                           stream=None, want=("dx", "dw", "db")):
+        """dX = G W, dW = G^T X and db = sum_m G[m, :] for encoder group `group`
+        on this encoder rank (SPEC.md:411 gradient path; tcgen05 CTA-pair GEMMs
+        of csrc/proj_bwd.cu: dX on the forward kernel with W^T, dW with MN-major
+        operands and db fused into it).  G = the returned gradient rows in
+        encoder order (`grad_return`, `grad_view`); x = the projector input
+        [>= rows, d_enc] (default: this rank's encoder output).  The row count
+        is `rows` (host) or, with `plan`, read on the device (no sync).  Rows
+        [M, round_up(M, 64)) of G and x are zeroed.  Returns (dx [M or max rows,
+        d_enc], dw [d_llm, d_enc], db [d_llm]) bf16, None for products not in
+        `want`."""
         assert self.projector and self.weight[group] is not None
-        dy = self.grad_view(group, rows)
-        x = self.enc_view(group, rows) if x is None else x
-        dx = dy @ self.weight[group]
-        dw = dy.t() @ x
-        db = dy.float().sum(0).to(torch.bfloat16)
+        self._ensure_grad()
+        dev, L = self.device, _lib.lib()
+        K, N = self.d_enc[group], self.d_llm
+        X = self.enc_out[group].view(-1, K) if x is None else x
+        assert X.dtype == torch.bfloat16 and X.is_contiguous() and X.shape[1] == K
+        m_max = min(self.max_rows, X.shape[0])
+        if plan is not None:
+            m_dev = plan.ptr + plan.layout.header + 8 * (_lib.H_RECV_ROWS0 + group)
+        else:
+            if rows is None or rows > m_max:
+                raise ValueError(f"rows {rows} must be given and <= {m_max}")
+            m_dev = 0
+            m_max = rows
+        G = self.grad[group].tensor[: self.max_rows * N * 2].view(torch.bfloat16).view(-1, N)
+        ws_need = L.mux_proj_backward_workspace(K, N, self.num_sms)
+        ws = getattr(self, "_bwd_ws", None)
+        if ws is None or ws.numel() < ws_need:
+            ws = self._bwd_ws = torch.empty(ws_need, dtype=torch.uint8, device=dev)
+        dx = torch.empty(max(m_max, 1), K, dtype=torch.bfloat16, device=dev) \
+            if "dx" in want else None
+        dw = torch.empty(N, K, dtype=torch.bfloat16, device=dev) if "dw" in want else None
+        db = torch.empty(N, dtype=torch.bfloat16, device=dev) if "db" in want else None
+        _lib.check(L.mux_proj_backward(
+            G.data_ptr(), X.data_ptr(), self.weight[group].data_ptr(), m_max, m_dev or None, K,
+            N, dx.data_ptr() if dx is not None else None,
+            dw.data_ptr() if dw is not None else None, db.data_ptr() if db is not None else None,
+            ws.data_ptr(), ws.numel(), self.num_sms, _stream_ptr(stream)), "mux_proj_backward")
+        if dx is not None and plan is None:
+            dx = dx[:rows]
         return dx, dw, db
 
     def grad_view(self, group: int, rows: int) -> torch.Tensor:

@@ -137,13 +137,16 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
              row_bytes_ret=(8192, 8192), chunk_bytes: int = DEFAULT_CHUNK_BYTES,
              ret_mode: int = _lib.RET_FINAL, row_bytes_grad=None, lssp_sp: int = 0,
              lssp_eta: int = 0, reshard: str = "ulysses", cp_threshold: int = 0,
-             text_embed: bool = False) -> PlanCfg:
+             text_embed: bool = False, reorder_group: int = 0, cost=None) -> PlanCfg:
     """One step's planner configuration (include/mux_b200.h mux_plan_cfg).
     lssp_sp > 0 turns on the LSSP eta split (samples longer than lssp_eta are
     encoded as token shards over groups of lssp_sp ranks; oracle/lssp.py).
     reshard: LLM placement over each replica's sp ranks, "ulysses" (uniform
     shards) or "cp_hybrid" (long samples split, short ones whole by LPT;
-    oracle/cphybrid.py), cp_threshold 0 = capacity / sp."""
+    oracle/cphybrid.py), cp_threshold 0 = capacity / sp.  reorder_group: ranks
+    per reorder group (0 = the whole world).  cost: None (token
+    counts) or per-encoder-group (lin, quad) with cost = lin L + quad L^2 —
+    costs.flops_forward, see costs.encoder_cost_params."""
     if reshard not in _lib.RESHARD:
         raise ValueError(f"unknown reshard variant {reshard!r}")
     if method not in METHODS:
@@ -163,6 +166,13 @@ def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int
     c.lssp_sp, c.lssp_eta = int(lssp_sp), int(lssp_eta)
     c.reshard, c.cp_threshold = _lib.RESHARD[reshard], int(cp_threshold)
     c.text_embed = int(bool(text_embed))
+    c.reorder_group = int(reorder_group)
+    if cost is None:
+        c.cost_model = _lib.COST_TOKENS
+    else:
+        c.cost_model = _lib.COST_FLOPS
+        for g in range(_lib.N_GROUPS):
+            c.cost_lin[g], c.cost_quad[g] = float(cost[g][0]), float(cost[g][1])
     return c
 
 

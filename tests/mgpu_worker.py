@@ -134,11 +134,12 @@ def main():
     sp = cfg["sp"] if world % cfg["sp"] == 0 and world >= cfg["sp"] else 1
     dp = world // sp
     gbs = cfg["gbs_per_replica"] * dp
+    full = "full" in sys.argv  # the bench's real widths (d_enc 1280, d_llm 4096)
     d_in = (20, 8) if narrow else configs.D_IN
-    d_llm = 64 if narrow else 512
+    d_llm = 64 if narrow else (configs.D_LLM if full else 512)
     descs = owork.descs_from_config(configs.DATASETS, cfg["datasets"])
     carry, seen = None, {}
-    d_enc = (256, 256)
+    d_enc = tuple(configs.D_ENC) if full else (256, 256)
     if proj and sp != 1:
         sp, dp = 1, world
         gbs = cfg["gbs_per_replica"] * dp

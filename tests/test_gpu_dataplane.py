@@ -230,3 +230,100 @@ def test_all_text_step_moves_no_modality_rows(cuda_device):
                        llm)
     got = path.llm_view(n).cpu().view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(got, llm[0])
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_streaming_pipeline_matches_list_form(cuda_device, overlap):
+    """run_pipeline(n=, prepare=): every step uploaded from pinned host memory
+    into one of two reused device slots on a copy stream (the bench's e2e form),
+    slots released through path.step_done; recv windows and LLM rows of every
+    step equal the list form's, also across two calls issued without a sync."""
+    from paper_2605_08962_b200.dataplane import MuxPath
+    steps = [(st, t) for nm, st, t, _ in golden_steps() if nm == "target1" and st["world"] == 1]
+    steps = (steps * 2)[:6]
+    cap, gbs = configs.CAPACITY, steps[0][0]["gbs"]
+    d_in, d_llm = (20, 8), 64
+    tables = [to_table(t) for _, t in steps]
+    os_ = [oplan.plan_step(t, cap, gbs, 1, 1, 1, 1, "lpt") for _, t in steps]
+    host_ar = [[payload(max(int(o["arena_rows"][0, g]), 1), d_in[g], 300 + 7 * k + g)
+                .pin_memory() for g in range(2)] for k, o in enumerate(os_)]
+
+    def run(stream_form, calls):
+        path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_llm=d_llm,
+                       overlap_dispatch=overlap)
+        recv, llm = [], []
+
+        def encoder(k, p, s):
+            o = os_[len(recv)]
+            recv.append([path.recv_view(g, int(o["recv_rows"][0, g])).clone() for g in range(2)])
+            path.encode_standin(p, dtab_of[len(recv) - 1], s)
+
+        def after(k, p, s):
+            llm.append(path.llm_view(int(os_[len(llm)]["llm_rows"][0])).clone())
+
+        dtab_of = {}
+        if not stream_form:
+            tabs = [planner.DeviceTable(t, "cuda") for t in tables]
+            for k, d in enumerate(tabs):
+                dtab_of[k] = d
+            path.run_pipeline([(tabs[k], [a.cuda() for a in host_ar[k]]) for k in range(6)],
+                              encoder=encoder, after_step=after)
+        else:
+            up = torch.cuda.Stream()
+            blobs = [torch.from_numpy(t.blob()).pin_memory() for t in tables]
+            slot_tab = [torch.empty(max(b.numel() for b in blobs), dtype=torch.int64,
+                                    device="cuda") for _ in range(2)]
+            slot_ar = [[torch.empty(max(h[g].numel() for h in host_ar), dtype=torch.bfloat16,
+                                    device="cuda") for g in range(2)] for _ in range(2)]
+            freed = [None, None]
+            base = [0]
+
+            def prepare(k):
+                j = base[0] + k
+                slot = j % 2
+                if freed[slot] is not None:
+                    up.wait_event(freed[slot])
+                with torch.cuda.stream(up):
+                    b = slot_tab[slot][:blobs[j].numel()]
+                    b.copy_(blobs[j], non_blocking=True)
+                    ars = []
+                    for g in range(2):
+                        h = host_ar[j][g]
+                        a = slot_ar[slot][g][:h.numel()].view(h.shape)
+                        a.copy_(h, non_blocking=True)
+                        ars.append(a)
+                ev = torch.cuda.Event()
+                ev.record(up)
+                dtab_of[j] = planner.DeviceTable.from_blob(tables[j], b)
+                return dtab_of[j], ars, ev
+
+            def after_s(k, p, s):
+                after(k, p, s)
+                if path.step_done is not None:
+                    s.wait_event(path.step_done)
+                e = torch.cuda.Event()
+                e.record(s)
+                freed[(base[0] + k) % 2] = e
+
+            per = 6 // calls
+            for c in range(calls):  # no synchronisation between the calls
+                base[0] = c * per
+                path.run_pipeline(n=per, prepare=prepare, encoder=encoder, after_step=after_s)
+        torch.cuda.synchronize()
+        return recv, llm
+
+    want_recv, want_llm = run(False, 1)
+    for k, ((st, t), o) in enumerate(zip(steps, os_)):  # the list form against the oracle
+        ar = [[a.view(torch.int16).numpy().view(np.uint16) for a in host_ar[k]]]
+        recv, _, llm = odp.run_world(o, t, 1, ar, d_in, (d_llm, d_llm), d_llm)
+        for g in range(2):
+            assert np.array_equal(want_recv[k][g].cpu().view(torch.int16).numpy()
+                                  .view(np.uint16), recv[0][g]), (k, g)
+        assert np.array_equal(want_llm[k].cpu().view(torch.int16).numpy().view(np.uint16),
+                              llm[0]), k
+    for calls in (1, 2):
+        got_recv, got_llm = run(True, calls)
+        for k in range(6):
+            for g in range(2):
+                assert torch.equal(got_recv[k][g], want_recv[k][g]), (calls, k, g)
+            assert torch.equal(got_llm[k], want_llm[k]), (calls, k)

@@ -6,7 +6,7 @@ import pytest
 from oracle import dataplane as odp
 from oracle import planner as oplan
 from oracle import workload as owork
-from paper_2605_08962_b200 import configs, planner, workload as W, balance
+from paper_2605_08962_b200 import balance, configs, costs, planner, workload as W
 from tests.helpers import golden, golden_steps, oracle_plan, random_table
 
 pytestmark = pytest.mark.gpu
@@ -18,10 +18,12 @@ def to_table(t):
                              int(t["n_carry_seqs"]), np.asarray(t["chunk_off"], np.int32))
 
 
-def device_plan(t, cap, gbs, dp, sp, world, me, method="lpt", pooled=False):
+def device_plan(t, cap, gbs, dp, sp, world, me, method="lpt", pooled=False, reorder_group=0,
+                cost=None):
     table = to_table(t)
     cfg = planner.make_cfg(table, cap, gbs, dp, sp, world, 1, method, pooled, me,
-                           row_bytes_in=(1176, 1024), row_bytes_ret=(8192, 8192))
+                           row_bytes_in=(1176, 1024), row_bytes_ret=(8192, 8192),
+                           reorder_group=reorder_group, cost=cost)
     plan = planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
     plan.check(table)
     return plan.host()
@@ -59,6 +61,36 @@ def test_plan_matches_oracle_on_golden_steps(cuda_device, method):
             assert_plan_equal(d, o, t, me)
             n += 1
     assert n > 20
+
+
+FLOPS = tuple(costs.encoder_cost_params(costs.ModelSpec(f"enc{g}", costs.ModelKind.ENCODER,
+                                                       p, layers, hidden, 16))
+              for g, (p, layers, hidden) in enumerate(configs.ENCODER_SHAPES))
+
+
+@pytest.mark.parametrize("method", ["lpt", "kk", "lpt_local", "lpt_local_rw"])
+@pytest.mark.parametrize("reorder_group,cost", [(2, None), (4, None), (0, FLOPS), (2, FLOPS),
+                                                (1, None)])
+def test_reorder_groups_and_flops_costs_match_oracle(cuda_device, method, reorder_group, cost):
+    """Reorder groups of consecutive ranks and the
+    flops-weighted cost (costs.py:108-124): every 4- and 8-rank golden step,
+    every rank's plan bit-exact; samples stay inside their origin's group."""
+    n = 0
+    for name, st, t, _ in golden_steps():
+        world, dp = st["world"], st["dp"]
+        if world < 4 or (reorder_group and world % reorder_group):
+            continue
+        o = oplan.plan_step(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, 1, method,
+                            reorder_group=reorder_group, cost=cost)
+        rg = reorder_group or world
+        e = o["enc"] >= 0
+        assert np.array_equal(o["enc"][e] // rg, o["origin"][e] // rg)
+        for me in range(world):
+            d = device_plan(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, me, method,
+                            reorder_group=reorder_group, cost=cost)
+            assert_plan_equal(d, o, t, me)
+            n += 1
+    assert n >= 8
 
 
 def test_plan_matches_oracle_random_tables(cuda_device):

@@ -222,3 +222,49 @@ def test_pipelined_ring_matches_oracle(cuda_device, overlap):
             ref[dst_row:dst_row + rows] = x[off:off + rows].float() @ Ws[q].float().t()
         err = (outs[k] - ref).abs()
         assert bool((err <= RTOL * ref.abs() + ATOL).all()), f"step {k}"
+
+
+def test_captured_step_graphs_match_oracle(cuda_device):
+    """MuxPath.capture_steps (bench --graphs 1): one CUDA graph per distinct step
+    (plan of step i+1 on the side stream beside step i's dispatch + projector);
+    replayed steps give the projected rows of the fp32 reference."""
+    from oracle import dataplane as odp
+    from oracle import planner as oplan
+    from paper_2605_08962_b200 import configs, planner
+    from paper_2605_08962_b200.dataplane import MuxPath
+    from tests.helpers import golden_steps
+    from tests.test_gpu_planner import to_table
+
+    steps = [(st, t) for nm, st, t, _ in golden_steps() if nm == "target1" and st["world"] == 1]
+    steps = steps[:2]
+    cap, gbs = configs.CAPACITY, steps[0][0]["gbs"]
+    d_in, d_enc, d_llm = configs.D_IN, configs.D_ENC, 512
+    path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_enc=d_enc, d_llm=d_llm,
+                   projector=True, method="lpt")
+    g = torch.Generator().manual_seed(8)
+    Ws = [(torch.randn(d_llm, d_enc[k], generator=g) / d_enc[k] ** 0.5).to(torch.bfloat16).cuda()
+          for k in range(2)]
+    for k in range(2):
+        path.set_projector(k, Ws[k], None)
+    tabs = [planner.DeviceTable(to_table(t), "cuda") for _, t in steps]
+    os_ = [oplan.plan_step(t, cap, gbs, 1, 1, 1, 1, "lpt") for _, t in steps]
+    arenas = [[torch.zeros(max(int(o["arena_rows"][0, k]), 1), d_in[k], dtype=torch.bfloat16,
+                           device="cuda") for k in range(2)] for o in os_]
+    graphs = path.capture_steps(tabs, arenas)
+    graphs.prime(0)
+    for i, ((st, t), o) in enumerate(zip(steps, os_)):
+        path.zero_llm()
+        path.encode_standin(graphs.plans[i], tabs[i])
+        graphs.replay(i)
+        torch.cuda.synchronize()
+        n = int(o["llm_rows"][0])
+        got = path.llm_view(n).float()
+        ref = torch.zeros(n, d_llm, device="cuda")
+        for (j, src, dst_rank, dst_row, rows) in o["pieces"]:
+            q = int(o["group"][j])
+            x = torch.from_numpy(odp.standin(int(t["ids"][j]), int(t["lens"][j]), d_enc[q])
+                                 .view(np.int16)).view(torch.bfloat16).cuda()
+            off = src - int(o["enc_off"][j])
+            ref[dst_row:dst_row + rows] = x[off:off + rows].float() @ Ws[q].float().t()
+        err = (got - ref).abs()
+        assert bool((err <= RTOL * ref.abs() + ATOL).all()), f"graph step {i}"

@@ -5,7 +5,7 @@ import pytest
 
 from oracle import planner as oplan
 from oracle import workload as owork
-from paper_2605_08962_b200 import configs
+from paper_2605_08962_b200 import configs, costs
 from tests.helpers import golden, golden_steps, oracle_plan, random_table
 
 
@@ -400,3 +400,47 @@ def test_cphybrid_threshold_monotone():
             assert prev is None or sharded <= prev
             prev = sharded
             assert c["shard_len"].sum(axis=1).tolist() == o["fills"][:st["gbs"]].tolist()
+
+
+def test_flops_cost_equals_reference_flops_forward():
+    """The planner's cost lin L + quad L^2 equals costs.flops_forward(spec, L, L)
+    (reference costs.py:108-124: encoder seq_len = L) bit for bit."""
+    spec = costs.ModelSpec("vit", costs.ModelKind.ENCODER, *configs.ENCODER_SHAPES[0], 16)
+    lin, quad = costs.encoder_cost_params(spec)
+    for L in (0, 1, 7, 255, 4096, 16384):
+        assert oplan.sample_cost(L, 0, ((lin, quad), (lin, quad))) == \
+            costs.flops_forward(spec, L, max(L, 1)) * (L > 0)
+
+
+def test_reorder_groups_keep_samples_in_their_group():
+    """a ReorderGroup is a block of consecutive ranks; samples move
+    only inside their origin's group, group = world reproduces the default plan,
+    and groups of one rank move nothing (the locality end of SPEC.md:433's
+    trade); each pool's loads stay LPT-balanced inside every group."""
+    n = 0
+    for name, st, t, _ in golden_steps():
+        world, dp = st["world"], st["dp"]
+        if world < 4:
+            continue
+        base = oplan.plan_step(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, 1, "lpt")
+        same = oplan.plan_step(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, 1, "lpt",
+                               reorder_group=world)
+        assert np.array_equal(base["enc"], same["enc"])
+        for rg in (world, world // 2, 1):
+            o = oplan.plan_step(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, 1, "lpt",
+                                reorder_group=rg)
+            e = o["enc"] >= 0
+            assert np.array_equal(o["enc"][e] // rg, o["origin"][e] // rg)
+            if rg == 1:
+                assert np.array_equal(o["enc"][e], o["origin"][e])
+            for q in range(world // rg):  # LPT bound inside each group and encoder group
+                for g in range(2):
+                    sel = e & (o["group"] == g) & (o["origin"] // rg == q)
+                    if not sel.any() or rg == 1:
+                        continue
+                    w = np.asarray(t["lens"])[sel]
+                    loads = o["recv_rows"][q * rg:(q + 1) * rg, g]
+                    assert loads.sum() == w.sum()
+                    assert loads.max() <= w.sum() / rg + w.max()  # greedy list-scheduling bound
+        n += 1
+    assert n >= 2
