@@ -479,6 +479,10 @@ def measure(name, args, ctx, primary=True):
               for j, nm in enumerate(("plan_ms", "pack_dispatch_ms",
                                       "projector_scatter_ms" if projector else "return_scatter_ms",
                                       "grad_return_ms"))}
+    backward = None
+    if projector and not path.staged:  # projector backward, after grad_return
+        backward = projector_backward_stage(path, dtabs, steps_idx_of(args, n_distinct),
+                                            plans_info, dy, stream, ctx)
     # dominant kernel = the return kernel (return+scatter copy, or the projector
     # GEMM), CUDA events on its stream around the launch, over the timed steps
     dom_ms = [a.elapsed_time(b) for a, b in ev_dom] if not graphs else \
@@ -568,6 +572,7 @@ def measure(name, args, ctx, primary=True):
         "roofline": roof,
         "exchange": exchange_summary(plans_info, steps_idx, rank),
         "stages": stages,
+        "backward": backward,
         "gpu_launches": launches * args.steps,
         "host_enqueue_ms_per_step": host_ms / args.steps,
         "e2e": e2e,
@@ -579,6 +584,45 @@ def measure(name, args, ctx, primary=True):
         if world == 1:
             line["cpu_baseline"] = cpu_baseline(name, tables[0], projector, world, args.method)
     return line
+
+
+def steps_idx_of(args, n_distinct):
+    return [(args.warmup + k) % n_distinct for k in range(args.steps)]
+
+
+def projector_backward_stage(path, dtabs, steps_idx, plans_info, dy, stream, ctx):
+    """dX = G W, dW = G^T X, db (csrc/proj_bwd.cu) of every encoder group after
+    each step's gradient return, timed with CUDA events (its own pass, not in
+    the headline step); roofline: 4 M d_enc d_llm FLOPs per group."""
+    import torch
+
+    from paper_2605_08962_b200 import _lib
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in steps_idx]
+    groups = [g for g in range(2) if path.weight[g] is not None]
+    for k, i in enumerate([steps_idx[0]] + list(steps_idx)):  # one warm-up step
+        p = path.plan(dtabs[i], stream)
+        path.grad_return(p, dy, stream)
+        a = ev[k - 1] if k else None
+        if a:
+            a[0].record(stream)
+        for g in groups:
+            if plans_info[i]["recv"][g]:
+                path.projector_backward(g, plan=p, stream=stream)
+        if a:
+            a[1].record(stream)
+    torch.cuda.synchronize()
+    path.check_wait()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    flops = np.mean([sum(4.0 * plans_info[i]["recv"][g] * path.d_enc[g] * path.d_llm
+                         for g in groups) for i in steps_idx])
+    peak, why = choose_tensor_peak(None)
+    _, burst, _, _ = peaks()
+    return {"ms": ms, "tflops": flops / (ms / 1e3) / 1e12, "peak": burst,
+            "frac": flops / (ms / 1e3) / 1e12 / burst,
+            "what": "dX = G W (pair GEMM, W^T) + dW = G^T X with fused db (pair GEMM, MN-major) "
+                    "per encoder group, after the gradient return; frac of the burst bf16 peak",
+            "rank": ctx["rank"]}
 
 
 def nvlink_roofline(path, plans_info, steps_idx, ret_s, disp_ms, ctx, projector):

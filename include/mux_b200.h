@@ -270,6 +270,14 @@ int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t which,
 /* One contiguous 8-byte-aligned byte range with the same copy engine as
  * mux_segcopy (local or NVLink-peer dst/src); used by the NVLink probe. */
 int mux_copy_bytes(void* dst, const void* src, int64_t n, int32_t grid_ctas, void* stream);
+/* n byte ranges (device arrays dsts/srcs/bytes; max_bytes = the longest, known
+ * to the caller) in one launch, 32 KiB chunks dealt round-robin over the
+ * ranges so every destination is written concurrently.  mode 0: SM
+ * loads/stores (the segment-copy engine); mode 1: TMA bulk copies through
+ * shared memory (cp.async.bulk); ranges 16-byte aligned for mode 1.  The
+ * NVLink probe's all-to-all and engine A/B. */
+int mux_copy_ranges(int32_t n, void* const* dsts, const void* const* srcs, const int64_t* bytes,
+                    int64_t max_bytes, int32_t grid_ctas, int32_t mode, void* stream);
 /* cudaMemcpyAsync(cudaMemcpyDefault): the copy-engine comparator of the probe. */
 int mux_memcpy_async(void* dst, const void* src, int64_t n, void* stream);
 
@@ -375,14 +383,31 @@ int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int32_t n_grou
                                     uint64_t* epoch_ctr, uint64_t* const* e_flags_peers,
                                     uint64_t* e_epoch_ctr, const int32_t* poison, void* stream);
 
+/* Decentralized step metadata ("metadata all-gather";
+ * SPEC.md:400-402): every rank packs its loader's share of the step (carried
+ * sequences and drawn chunks, contiguous ranges in rank order) into a record
+ * of mux_meta_record_words(cap_rows, cap_chunks) int32 words:
+ *   [n_carry_rows, n_carry_seqs, n_chunk_rows, n_chunks], ids int64[cap_rows],
+ *   lens int32[cap_rows], mods int32[cap_rows], carry seq (local) int32[cap_rows],
+ *   chunk sizes int32[cap_chunks]   (rows: carry rows first, then chunk rows).
+ * After an all-gather of the records (world of them, rank order),
+ * mux_assemble_table writes the global step-table blob (ids int64[S] | lens |
+ * mods | carry_seq | chunk_off, the layout mux_plan_step reads) in the order
+ * the centralized generate_batch produces (workload.py:281-305).  *err
+ * (device int32, zero on entry) is set to 1 if a record is malformed or
+ * out_words is too small. */
+int64_t mux_meta_record_words(int32_t cap_rows, int32_t cap_chunks);
+int mux_assemble_table(const int32_t* records, int32_t world, int32_t cap_rows, int32_t cap_chunks,
+                       int64_t* out_blob, int64_t out_words, int32_t* err, void* stream);
+
 /* Backward of the projector (no reference kernel; the gradient path of
  * SPEC.md:411 and PAPER.md:1114), on the encoder rank after the gradient
  * return: G bf16 [M_max, N] = dL/dY of the encoder rows in encoder order,
  * X bf16 [M_max, K] = the projector input, W bf16 [N, K] the weight.
  *   dX bf16 [M_max, K] = G . W        (rows < M written)
  *   dW bf16 [N, K]     = G^T . X      (fp32 accumulation, deterministic)
- *   db bf16 [N]        = sum_m G[m,:] (fused into the dW launch; NULL = skip)
- * M = *M_dev clamped to M_max (M_dev NULL: M_max).  dX or dW may be NULL to
+ *   db bf16 [N]        = sum_m G[m,:] (one pass over G, deterministic; NULL = skip)
+ * M = *M_dev clamped to M_max (M_dev NULL: M_max).  dX, dW or db may be NULL to
  * skip that product.  Rows [M, round_up(M, 64)) of G and X are zeroed.
  * tcgen05 CTA-pair GEMMs (MN-major operands for dW); K % 256 == 0,
  * N % 256 == 0.  workspace >= mux_proj_backward_workspace(K, N, num_sms)

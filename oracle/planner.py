@@ -454,3 +454,33 @@ def plan_reshard(sequences, n_ranks, variant, cp_threshold=None, capacity=None):
         else:
             raise ValueError(f"unknown reshard variant {variant!r}")
     return smap, loads
+
+
+def assemble_records(records, cap_rows, cap_chunks):
+    """Global step table from every rank's metadata record (rank order) — the
+    CPU restatement of mux_assemble_table (csrc/meta.cu) for the decentralized
+    metadata all-gather.  Builder-defined record layout:
+    [n_carry_rows, n_carry_seqs, n_chunk_rows, n_chunks], ids int64[cap],
+    lens, mods, local carry seq int32[cap], chunk sizes int32[cap_chunks]."""
+    lens, mods, ids, cseq = [], [], [], []
+    klens, kmods, kids, sizes = [], [], [], []
+    q0 = 0
+    for rec in records:
+        rec = np.asarray(rec, np.int32)
+        ncr, ncs, nkr, nk = (int(x) for x in rec[:4])
+        rid = rec[4:4 + 2 * cap_rows].view(np.int64)
+        o = 4 + 2 * cap_rows
+        rl, rm = rec[o:o + cap_rows], rec[o + cap_rows:o + 2 * cap_rows]
+        rc, rs = rec[o + 2 * cap_rows:o + 3 * cap_rows], rec[o + 3 * cap_rows:]
+        ids += rid[:ncr].tolist(); lens += rl[:ncr].tolist(); mods += rm[:ncr].tolist()
+        cseq += (rc[:ncr] + q0).tolist()
+        kids += rid[ncr:ncr + nkr].tolist(); klens += rl[ncr:ncr + nkr].tolist()
+        kmods += rm[ncr:ncr + nkr].tolist(); sizes += rs[:nk].tolist()
+        q0 += ncs
+    nc = len(ids)
+    chunk_off = [nc]
+    for n in sizes:
+        chunk_off.append(chunk_off[-1] + n)
+    return dict(lens=np.array(lens + klens, np.int64), mods=np.array(mods + kmods, np.int64),
+                ids=np.array(ids + kids, np.int64), carry_seq=np.array(cseq, np.int64),
+                n_carry_seqs=q0, chunk_off=chunk_off)

@@ -84,6 +84,7 @@ _SIGS = [
                                  C.c_int32, _P, _P, _P, _P, _P]),
     ("mux_copy_bytes", C.c_int, [_P, _P, C.c_int64, C.c_int32, _P]),
     ("mux_memcpy_async", C.c_int, [_P, _P, C.c_int64, _P]),
+    ("mux_copy_ranges", C.c_int, [C.c_int32, _P, _P, _P, C.c_int64, C.c_int32, C.c_int32, _P]),
     ("mux_signal", C.c_int, [C.c_int32, C.c_int32, _P, _P, _P]),
     ("mux_wait", C.c_int, [C.c_int32, _P, _P, C.c_int32, _P, _P]),
     ("mux_signal_ex", C.c_int, [C.c_int32, C.c_int32, _P, _P, C.c_int32, _P]),
@@ -103,6 +104,9 @@ _SIGS = [
     ("mux_proj_scatter_grouped_signal", C.c_int, [C.POINTER(ProjGroup), C.c_int32, C.c_int32,
                                                   _P, C.c_int32, C.c_int32, C.c_int32, _P, _P,
                                                   _P, _P, _P, _P, _P]),
+    ("mux_meta_record_words", C.c_int64, [C.c_int32, C.c_int32]),
+    ("mux_assemble_table", C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64, _P,
+                                     _P]),
     ("mux_proj_backward_workspace", C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
     ("mux_proj_backward", C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P, _P,
                                     _P, C.c_size_t, C.c_int32, _P]),

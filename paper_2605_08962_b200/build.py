@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libmuxb200.so")
 SOURCES = ["capi.cu", "plan.cu", "lssp.cu", "reshard.cu", "segcopy.cu", "proj_gemm.cu",
-           "proj_bwd.cu"]
+           "proj_bwd.cu", "meta.cu"]
 HEADERS = ["mux_common.cuh", "umma.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

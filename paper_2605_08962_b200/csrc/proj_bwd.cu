@@ -10,8 +10,11 @@
 //                              wt_transpose_kernel writes into the workspace
 //   dW = G^T . X      [N, K]   dw_pair_kernel below: reduction over the M rows,
 //                              both operands MN-major straight from G and X
-//   db = sum_m G[m,:] [N]      a sum warp of dw_pair_kernel adds up the G tiles
-//                              the MMAs already staged (tiles with k-block 0)
+//   db = sum_m G[m,:] [N]      colsum_kernel (fp32 partials over 148 row ranges,
+//                              summed in order): one HBM pass over G.  A sum
+//                              warp reading the staged G tiles inside
+//                              dw_pair_kernel was measured first: holding each
+//                              stage for it halved the GEMM (0.85 vs 0.38 ms)
 //
 // dw_pair_kernel: CTA pairs (cta_group::2), M256 (rows of dW = N) x N256
 // (columns = K) tiles, 64-row K-blocks of G / X by TMA (two 64x64 boxes per
@@ -26,6 +29,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "mux_common.cuh"
@@ -41,8 +45,7 @@ constexpr int STAGES = 4;
 constexpr int HALF_BYTES = 128 * BK * 2;          // one CTA's half of an operand: 16 KB
 constexpr int STAGE_BYTES = 2 * HALF_BYTES;       // A half + B half
 constexpr int kEpiWarps = 8;
-constexpr int kSumWarp = 2 + kEpiWarps;           // warp 10
-constexpr int kThreads = 32 * (kSumWarp + 1);     // 352
+constexpr int kThreads = 32 * (2 + kEpiWarps);    // 320
 constexpr int kStagingBytes = kEpiWarps * 32 * 128;
 constexpr int kSmem = STAGES * STAGE_BYTES + 512 + kStagingBytes + 1024;
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
@@ -54,9 +57,9 @@ struct Params {
   const int64_t* M_dev;
   int N, K;
   uint16_t* dW;      // [N, K] bf16
-  uint16_t* db;      // [N] bf16 or NULL
   float* part;       // [pairs][TN][TK] fp32 partials of split tiles
-  float* part_db;    // [pairs][TN]
+  int prefetch;      // L2 prefetch distance in K-blocks (0: off)
+  int evict_last;    // L2 policy of the operand loads: 1 evict_last, 0 evict_normal
 };
 
 // One unit of a pair's work: tile, K-block range, partial slot (-1: direct).
@@ -87,8 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1) dw_pair_kernel(const __grid_const
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* mdone = empty + STAGES;
-  uint64_t* tfull = mdone + STAGES;
+  uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -116,8 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) dw_pair_kernel(const __grid_const
     tma_prefetch(&P.tx);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);  // the MMA commit + this CTA's sum warp
-      mbar_init(&mdone[s], 1);
+      mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -134,15 +135,32 @@ __global__ void __launch_bounds__(kThreads, 1) dw_pair_kernel(const __grid_const
   if (warp == 0) {
     // ---- TMA producer: this CTA's 128 rows of A (= G columns) and 128
     // columns of B (= X columns) per K-block, each as two 64 x 64 boxes
+    // Every pair walks the same M rows at the same pace, so each K-block is
+    // first requested by all pairs at once: the loads would wait for HBM at
+    // every stage.  An L2 prefetch `prefetch` K-blocks ahead hides that.
     if (lane == 0) {
-      const uint64_t pol = policy_evict_last();
+      const uint64_t pol = P.evict_last ? policy_evict_last() : policy_evict_normal();
+      const int D = P.prefetch;
       int stage = 0;
       uint32_t phase = 0;
       for (int w = 0; w < n_items; ++w) {
         const Item it = sp.item(cid, w);
         const int n0 = (it.tile / NK) * TN + (int)rank * 128;
         const int k0 = (it.tile % NK) * TK + (int)rank * 128;
+        for (int kb = it.kb0; kb < it.kb0 + D && kb < it.kb1; ++kb) {
+          tma_prefetch_l2_2d(&P.tg, n0, kb * BK);
+          tma_prefetch_l2_2d(&P.tg, n0 + 64, kb * BK);
+          tma_prefetch_l2_2d(&P.tx, k0, kb * BK);
+          tma_prefetch_l2_2d(&P.tx, k0 + 64, kb * BK);
+        }
         for (int kb = it.kb0; kb < it.kb1; ++kb) {
+          if (D && kb + D < it.kb1) {
+            const int mp = (kb + D) * BK;
+            tma_prefetch_l2_2d(&P.tg, n0, mp);
+            tma_prefetch_l2_2d(&P.tg, n0 + 64, mp);
+            tma_prefetch_l2_2d(&P.tx, k0, mp);
+            tma_prefetch_l2_2d(&P.tx, k0 + 64, mp);
+          }
           mbar_wait_bounded(&empty[stage], phase ^ 1, false);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
@@ -181,7 +199,6 @@ __global__ void __launch_bounds__(kThreads, 1) dw_pair_kernel(const __grid_const
           for (int k = 0; k < BK / 16; ++k)  // 16 rows of G / X = 2048 B per step
             mma_bf16_pair(d, ad + 128 * k, bd + 128 * k, idesc, (kb > it.kb0 || k) ? 1u : 0u);
           mma_commit_pair(&empty[stage], 0x3);
-          mma_commit_pair(&mdone[stage], 0x3);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -194,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) dw_pair_kernel(const __grid_const
         }
       }
     }
-  } else if (warp < kSumWarp) {
+  } else {
     // ---- epilogue: TMEM -> bf16 dW rows (whole tiles) or fp32 partials
     const int quarter = warp & 3, colgrp = (warp - 2) >> 2;
     uint4* stg = reinterpret_cast<uint4*>(smem + STAGES * STAGE_BYTES + 512) +
@@ -277,49 +294,6 @@ __global__ void __launch_bounds__(kThreads, 1) dw_pair_kernel(const __grid_const
         }
       }
     }
-  } else {
-    // ---- sum warp: db = column sums of G over the staged K-blocks of tiles
-    // whose column block is 0.  Lane l owns this CTA's G columns 4l..4l+3:
-    // box (l >> 4), 16-byte chunk (l & 15) >> 1, half l & 1 of it.
-    const int box = lane >> 4, chunk = (lane & 15) >> 1, half = lane & 1;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int w = 0; w < n_items; ++w) {
-      const Item it = sp.item(cid, w);
-      const bool want = P.db != nullptr && (it.tile % NK) == 0;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      for (int kb = it.kb0; kb < it.kb1; ++kb) {
-        mbar_wait_bounded(&mdone[stage], phase, false);
-        if (want) {
-          const uint8_t* sa = smem + stage * STAGE_BYTES + box * (HALF_BYTES / 2);
-#pragma unroll 8
-          for (int r = 0; r < BK; ++r) {
-            const uint2 u = *reinterpret_cast<const uint2*>(
-                sa + (r >> 3) * 1024 + (r & 7) * 128 + ((chunk ^ (r & 7)) << 4) + half * 8);
-            s0 += __uint_as_float(u.x << 16);
-            s1 += __uint_as_float(u.x & 0xffff0000u);
-            s2 += __uint_as_float(u.y << 16);
-            s3 += __uint_as_float(u.y & 0xffff0000u);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      if (want) {
-        const int nl = (int)rank * 128 + 4 * lane;  // row of the tile
-        if (it.slot >= 0) {
-          *reinterpret_cast<float4*>(P.part_db + (int64_t)it.slot * TN + nl) =
-              make_float4(s0, s1, s2, s3);
-        } else {
-          const int n = (it.tile / NK) * TN + nl;
-          *reinterpret_cast<uint2*>(P.db + n) = make_uint2(pack_bf16(s0, s1), pack_bf16(s2, s3));
-        }
-      }
-    }
   }
   fence_before();
   __syncthreads();
@@ -329,8 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) dw_pair_kernel(const __grid_const
 }
 
 // Split tiles: dW[n, k] = sum over the S partials of its pairs, in chunk order.
-__global__ void dw_reduce_kernel(const float* part, const float* part_db, int T, int P, int N,
-                                 int K, uint16_t* dW, uint16_t* db) {
+__global__ void dw_reduce_kernel(const float* part, int T, int P, int N, int K, uint16_t* dW) {
   const int NK = K / TK;
   const int W1 = T / P, R = T - W1 * P;
   if (!R) return;
@@ -344,11 +317,59 @@ __global__ void dw_reduce_kernel(const float* part, const float* part_db, int T,
     for (int j = 0; j < S; ++j) s += part[((int64_t)(r + j * R) * TN + row) * TK + c];
     reinterpret_cast<__nv_bfloat16*>(dW)[(int64_t)n * K + k0 + c] = __float2bfloat16_rn(s);
   }
-  if (db && tile % NK == 0 && threadIdx.x == 0) {
-    float s = 0.f;
-    for (int j = 0; j < S; ++j) s += part_db[(int64_t)(r + j * R) * TN + row];
-    reinterpret_cast<__nv_bfloat16*>(db)[n] = __float2bfloat16_rn(s);
+}
+
+// db = column sums of G over its first M rows, deterministic: colsum_kernel
+// writes fp32 partials of kColsumSplits row ranges (8 columns per thread,
+// 16-byte loads), colsum_reduce_kernel adds them in range order.
+constexpr int kColsumSplits = 148;
+__global__ void __launch_bounds__(256) colsum_kernel(const uint16_t* G, int64_t M_max,
+                                                     const int64_t* M_dev, int N, float* part) {
+  int64_t M = M_max;
+  if (M_dev) {
+    const int64_t m = *M_dev;
+    M = m < M ? (m > 0 ? m : 0) : M;
   }
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c0 >= N) return;
+  const int64_t r0 = M * blockIdx.y / gridDim.y, r1 = M * (blockIdx.y + 1) / gridDim.y;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const uint16_t* p = G + r0 * N + c0;
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4, p += 4 * (int64_t)N) {
+    uint4 u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = __ldg(reinterpret_cast<const uint4*>(p + k * (int64_t)N));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s[2 * j] += __uint_as_float(w[j] << 16);
+        s[2 * j + 1] += __uint_as_float(w[j] & 0xffff0000u);
+      }
+    }
+  }
+  for (; r < r1; ++r, p += N) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      s[2 * j] += __uint_as_float(w[j] << 16);
+      s[2 * j + 1] += __uint_as_float(w[j] & 0xffff0000u);
+    }
+  }
+  float4* o = reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * N + c0);
+  o[0] = make_float4(s[0], s[1], s[2], s[3]);
+  o[1] = make_float4(s[4], s[5], s[6], s[7]);
+}
+
+__global__ void colsum_reduce_kernel(const float* part, int splits, int N, uint16_t* db) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  float s = 0.f;
+  for (int j = 0; j < splits; ++j) s += part[(int64_t)j * N + c];
+  reinterpret_cast<__nv_bfloat16*>(db)[c] = __float2bfloat16_rn(s);
 }
 
 // Zero rows [M, min(round_up(M, 64), M_max)) of a [M_max, width] bf16 buffer.
@@ -424,19 +445,20 @@ static int pairs_of(int num_sms) {
 }
 
 struct WsLayout {
-  size_t wt, part, part_db, bases, total;
+  size_t wt, part, bases, colsum, total;
 };
 
 static WsLayout ws_layout(int32_t K, int32_t N, int pairs) {
+
   WsLayout L;
   L.wt = 0;
   size_t o = ((size_t)K * N * 2 + 255) & ~size_t(255);
   L.part = o;
   o += ((size_t)pairs * TN * TK * 4 + 255) & ~size_t(255);
-  L.part_db = o;
-  o += ((size_t)pairs * TN * 4 + 255) & ~size_t(255);
   L.bases = o;  // device pointer table of the dX launch (one entry)
   o += 256;
+  L.colsum = o;  // db partials [kColsumSplits][N] fp32
+  o += ((size_t)kColsumSplits * N * 4 + 255) & ~size_t(255);
   L.total = o;
   return L;
 }
@@ -504,9 +526,16 @@ extern "C" int mux_proj_backward(const uint16_t* G, const uint16_t* X, const uin
     P.N = N;
     P.K = K;
     P.dW = dW;
-    P.db = db;
     P.part = reinterpret_cast<float*>(ws + L.part);
-    P.part_db = reinterpret_cast<float*>(ws + L.part_db);
+    static int pf = -1, el = -1;  // MUX_BWD_PREFETCH / MUX_BWD_EVICT_LAST (tuning)
+    if (pf < 0) {
+      const char* e = getenv("MUX_BWD_PREFETCH");
+      pf = e ? atoi(e) : 8;
+      const char* f = getenv("MUX_BWD_EVICT_LAST");
+      el = f ? atoi(f) : 0;
+    }
+    P.prefetch = pf;
+    P.evict_last = el;
     static bool attr = false;
     if (!attr) {
       MUX_CUDA(cudaFuncSetAttribute(dw_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -528,13 +557,16 @@ extern "C" int mux_proj_backward(const uint16_t* G, const uint16_t* X, const uin
     MUX_CUDA(cudaLaunchKernelEx(&lc, dw_pair_kernel, P));
     const int T = (N / TN) * (K / TK);
     if (T % pairs) {
-      dw_reduce_kernel<<<(T % pairs) * TN, 256, 0, s>>>(P.part, P.part_db, T, pairs, N, K, dW,
-                                                        db);
+      dw_reduce_kernel<<<(T % pairs) * TN, 256, 0, s>>>(P.part, T, pairs, N, K, dW);
       MUX_CUDA(cudaGetLastError());
     }
-  } else if (db) {
-    set_error("projector backward: db is computed with dW (pass dW too)");
-    return MUX_ERR_VALUE;
+  }
+  if (db) {
+    float* part = reinterpret_cast<float*>(ws + L.colsum);
+    colsum_kernel<<<dim3((N / 8 + 255) / 256, kColsumSplits), 256, 0, s>>>(G, M_max, M_dev, N,
+                                                                           part);
+    colsum_reduce_kernel<<<(N + 255) / 256, 256, 0, s>>>(part, kColsumSplits, N, db);
+    MUX_CUDA(cudaGetLastError());
   }
   return MUX_OK;
 }

@@ -223,6 +223,105 @@ __global__ void __launch_bounds__(kCopyThreads) copy_bytes_kernel(char* dst, con
     copy_block(dst + lo, src + lo, n - lo < CH ? n - lo : CH);
 }
 
+// ---------------------------------------------------------------------------
+// Multi-range copy (NVLink probe, copy-engine A/B): n ranges, 32 KiB chunks
+// dealt round-robin over the ranges so every destination is written at once.
+// mode 0: SM loads/stores (copy_block); mode 1: TMA bulk copies — each CTA
+// streams its chunks global -> shared (cp.async.bulk, mbarrier) -> global
+// (cp.async.bulk.global.shared::cta) through a ring of kBulkBufs buffers.
+// ---------------------------------------------------------------------------
+constexpr int kBulkChunk = 32768, kBulkBufs = 3;
+
+struct RangeArgs {
+  int n;
+  void* const* dst;
+  const void* const* src;
+  const int64_t* bytes;
+  int64_t max_chunks;  // chunks of the longest range
+};
+
+__device__ __forceinline__ bool range_chunk(const RangeArgs& a, int64_t c, char*& d, const char*& s,
+                                            int64_t& len) {
+  const int r = (int)(c % a.n);
+  const int64_t k = c / a.n;
+  const int64_t lo = k * kBulkChunk, b = a.bytes[r];
+  if (lo >= b) return false;
+  len = b - lo < kBulkChunk ? b - lo : kBulkChunk;
+  d = static_cast<char*>(a.dst[r]) + lo;
+  s = static_cast<const char*>(a.src[r]) + lo;
+  return true;
+}
+
+__global__ void __launch_bounds__(kCopyThreads) ranges_sm_kernel(RangeArgs a) {
+  const int64_t total = a.max_chunks * a.n;
+  for (int64_t c = blockIdx.x; c < total; c += gridDim.x) {
+    char* d;
+    const char* s;
+    int64_t len;
+    if (range_chunk(a, c, d, s, len)) copy_block(d, s, len);
+  }
+}
+
+__global__ void __launch_bounds__(32) ranges_bulk_kernel(RangeArgs a) {
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  __shared__ uint64_t bar[kBulkBufs];
+  if (threadIdx.x != 0) return;
+  const int64_t total = a.max_chunks * a.n;
+  // this CTA's chunks: c = blockIdx.x + j * gridDim.x, j = 0, 1, ...
+  for (int b = 0; b < kBulkBufs; ++b)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&bar[b])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto load = [&](int64_t j) {  // issue the load of this CTA's chunk j into buffer j % NB
+    const int b = (int)(j % kBulkBufs);
+    char* d;
+    const char* s;
+    int64_t len = 0;
+    const int64_t c = blockIdx.x + j * gridDim.x;
+    if (c >= total || !range_chunk(a, c, d, s, len)) len = 0;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(bulk_smem + b * kBulkChunk);
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&bar[b]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                 "r"((uint32_t)len)
+                 : "memory");
+    if (len)
+      asm volatile(
+          "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(sb),
+          "l"(s), "r"((uint32_t)len), "r"(mb)
+          : "memory");
+  };
+  const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  for (int64_t j = 0; j < kBulkBufs - 1 && j < mine; ++j) load(j);
+  for (int64_t j = 0; j < mine; ++j) {
+    if (j + kBulkBufs - 1 < mine) {
+      // buffer (j - 1) % NB is reused: the store of chunk j-1 must have read it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      load(j + kBulkBufs - 1);
+    }
+    const int b = (int)(j % kBulkBufs);
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&bar[b]);
+    const uint32_t par = (uint32_t)((j / kBulkBufs) & 1);
+    asm volatile(
+        "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(mb),
+        "r"(par)
+        : "memory");
+    char* d;
+    const char* s;
+    int64_t len;
+    const int64_t c = blockIdx.x + j * gridDim.x;
+    if (range_chunk(a, c, d, s, len)) {
+      const uint32_t sb = (uint32_t)__cvta_generic_to_shared(bulk_smem + b * kBulkChunk);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d), "r"(sb),
+                   "r"((uint32_t)len)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void signal_kernel(int me, int world, uint64_t* const* flags_peers,
                               uint64_t* epoch_ctr, int fence) {
   const int r = threadIdx.x;
@@ -575,6 +674,32 @@ extern "C" int mux_copy_bytes(void* dst, const void* src, int64_t n, int32_t gri
   const int grid = grid_ctas > 0 ? grid_ctas : num_sms() * 8;
   copy_bytes_kernel<<<grid, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<char*>(dst), static_cast<const char*>(src), n);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_copy_ranges(int32_t n, void* const* dsts, const void* const* srcs,
+                               const int64_t* bytes, int64_t max_bytes, int32_t grid_ctas,
+                               int32_t mode, void* stream) {
+  if (n <= 0 || !dsts || !srcs || !bytes || max_bytes < 0 || (mode != 0 && mode != 1)) {
+    set_error("mux_copy_ranges: n > 0, device arrays, max_bytes >= 0, mode 0 (SM) or 1 (TMA)");
+    return MUX_ERR_VALUE;
+  }
+  RangeArgs a{n, dsts, srcs, bytes, (max_bytes + kBulkChunk - 1) / kBulkChunk};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (mode == 0) {
+    ranges_sm_kernel<<<grid_ctas > 0 ? grid_ctas : num_sms() * 8, kCopyThreads, 0, s>>>(a);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      MUX_CUDA(cudaFuncSetAttribute(ranges_bulk_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kBulkBufs * kBulkChunk));
+      attr = true;
+    }
+    ranges_bulk_kernel<<<grid_ctas > 0 ? grid_ctas : num_sms() * 2, 32, kBulkBufs * kBulkChunk,
+                         s>>>(a);
+  }
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

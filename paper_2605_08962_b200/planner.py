@@ -79,6 +79,45 @@ class StepTable:
                          np.asarray(ids, np.int64), np.asarray(cseq, np.int32), len(carry),
                          np.asarray(off, np.int32))
 
+    def shard(self, rank: int, world: int) -> "StepTable":
+        """The share of this step a decentralized loader on `rank` holds
+        (PAPER.md:1104): carried sequences and drawn chunks split into `world`
+        contiguous ranges in rank order (numpy array_split); carry sequence ids
+        and chunk offsets are local.  gather_table reassembles the step."""
+        qs = np.array_split(np.arange(self.n_carry_seqs), world)[rank]
+        cs = np.array_split(np.arange(self.n_chunks), world)[rank]
+        q0 = int(qs[0]) if len(qs) else 0
+        carry = np.flatnonzero(np.isin(self.carry_seq, qs)) if len(qs) else np.zeros(0, np.int64)
+        rows = [int(i) for i in carry]
+        sizes = []
+        for c in cs:
+            lo, hi = int(self.chunk_off[c]), int(self.chunk_off[c + 1])
+            rows += range(lo, hi)
+            sizes.append(hi - lo)
+        rows = np.asarray(rows, np.int64)
+        off = np.concatenate([[len(carry)], len(carry) + np.cumsum(sizes, dtype=np.int64)])
+        return StepTable(self.lens[rows].astype(np.int32), self.mods[rows].astype(np.int32),
+                         self.ids[rows].astype(np.int64),
+                         (self.carry_seq[carry] - q0).astype(np.int32), len(qs),
+                         off.astype(np.int32))
+
+    def record(self, cap_rows: int, cap_chunks: int) -> np.ndarray:
+        """This shard as one metadata record (int32 words, include/mux_b200.h
+        mux_assemble_table) for the all-gather."""
+        S, nc, nch = self.S, self.n_carry, self.n_chunks
+        if S > cap_rows or nch > cap_chunks:
+            raise ValueError(f"shard of {S} rows / {nch} chunks exceeds the record capacity "
+                             f"{cap_rows} / {cap_chunks}")
+        rec = np.zeros(_lib.lib().mux_meta_record_words(cap_rows, cap_chunks), np.int32)
+        rec[:4] = (nc, self.n_carry_seqs, S - nc, nch)
+        rec[4:4 + 2 * cap_rows].view(np.int64)[:S] = self.ids
+        o = 4 + 2 * cap_rows
+        rec[o:o + S] = self.lens
+        rec[o + cap_rows:o + cap_rows + S] = self.mods
+        rec[o + 2 * cap_rows:o + 2 * cap_rows + nc] = self.carry_seq
+        rec[o + 3 * cap_rows:o + 3 * cap_rows + nch] = np.diff(self.chunk_off)
+        return rec
+
     def blob(self) -> np.ndarray:
         """One int64 array: ids | int32(lens, mods, carry_seq, chunk_off)."""
         S, nc, nch = self.S, self.n_carry, self.n_chunks
@@ -129,6 +168,66 @@ def _device_table_from_blob(table: StepTable, blob: torch.Tensor) -> "DeviceTabl
     dt.lens, dt.mods = base + 8 * S, base + 12 * S
     dt.carry_seq, dt.chunk_off = base + 16 * S, base + 16 * S + 4 * nc
     return dt
+
+
+class GatheredTable:
+    """Step table assembled on the device from every rank's metadata record:
+    the host holds only the sizes (what PlanCfg needs); the per-sample arrays
+    are read back from the device blob on demand (e.g. plan.check's error
+    message), never needed on the data path."""
+
+    def __init__(self, blob: torch.Tensor, S: int, n_carry: int, n_carry_seqs: int,
+                 n_chunks: int):
+        self.dev_blob, self.S, self.n_carry = blob, S, n_carry
+        self.n_carry_seqs, self.n_chunks = n_carry_seqs, n_chunks
+        self._host = None
+
+    def host(self) -> StepTable:
+        if self._host is None:
+            b = self.dev_blob.cpu().numpy()
+            S, nc, nch = self.S, self.n_carry, self.n_chunks
+            v = b[S:].view(np.int32)
+            self._host = StepTable(v[:S].copy(), v[S:2 * S].copy(), b[:S].copy(),
+                                   v[2 * S:2 * S + nc].copy(), self.n_carry_seqs,
+                                   v[2 * S + nc:2 * S + nc + nch + 1].copy())
+        return self._host
+
+    ids = property(lambda self: self.host().ids)
+    lens = property(lambda self: self.host().lens)
+    mods = property(lambda self: self.host().mods)
+    carry_seq = property(lambda self: self.host().carry_seq)
+    chunk_off = property(lambda self: self.host().chunk_off)
+
+
+def gather_table(shard: StepTable, device, group=None, cap_rows: int = 2048,
+                 cap_chunks: int = 64, stream=None) -> "DeviceTable":
+    """Decentralized metadata all-gather:
+    this rank's loader share -> one record -> all_gather_into_tensor over the
+    process group (NCCL over NVLink) -> mux_assemble_table on the device.  Only
+    the 4-word record headers come back to the host (PlanCfg's sizes); run it
+    on the planner's side stream one step ahead, as a loader prefetches."""
+    import torch.distributed as dist
+    L = _lib.lib()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    with torch.cuda.stream(s):
+        rec = torch.from_numpy(shard.record(cap_rows, cap_chunks)).to(device, non_blocking=True)
+        if world > 1:
+            allrec = torch.empty(world * rec.numel(), dtype=torch.int32, device=device)
+            dist.all_gather_into_tensor(allrec, rec, group=group)
+        else:
+            allrec = rec
+        hdr = allrec.view(world, -1)[:, :4].cpu().numpy().astype(np.int64)
+        nc, ncs, nk, nch = (int(x) for x in hdr.sum(0))
+        S = nc + nk
+        words = S + (2 * S + nc + nch + 1 + 1) // 2
+        blob = torch.empty(max(words, 1), dtype=torch.int64, device=device)
+        err = torch.zeros(1, dtype=torch.int32, device=device)
+        _lib.check(L.mux_assemble_table(allrec.data_ptr(), world, cap_rows, cap_chunks,
+                                        blob.data_ptr(), blob.numel(), err.data_ptr(),
+                                        s.cuda_stream), "mux_assemble_table")
+    table = GatheredTable(blob, S, nc, ncs, nch)
+    return _device_table_from_blob(table, blob)
 
 
 def make_cfg(table: StepTable, capacity: int, gbs: int = 0, dp: int = 1, sp: int = 1,

@@ -125,6 +125,8 @@ def main():
     lssp = "lssp" in sys.argv  # LSSP eta split: long samples sharded over encoder groups
     cp = "cp" in sys.argv  # CpHybrid LLM placement instead of Ulysses shards
     overlap = "overlap" in sys.argv  # run_pipeline with the overlapped dispatch
+    meta = "meta" in sys.argv  # step table from the decentralized metadata all-gather
+    rg = 2 if "rg2" in sys.argv else 0  # reorder groups of two ranks
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -149,7 +151,7 @@ def main():
                    projector_return="staged" if "staged" in sys.argv else "fused",
                    lssp_eta=2048 if lssp else None, lssp_sp=world if lssp else 1,
                    reshard="cp_hybrid" if cp else "ulysses", cp_threshold=2048 if cp else 0,
-                   overlap_dispatch=overlap)
+                   overlap_dispatch=overlap, reorder_group=rg)
     if proj:
         gw = torch.Generator().manual_seed(9)
         Ws = [(torch.randn(d_llm, d_enc[g], generator=gw) / d_enc[g] ** 0.5).to(torch.bfloat16)
@@ -176,7 +178,8 @@ def main():
         carry = rest
         for method in (("lpt_local",) if proj else ("lpt", "kk", "lpt_local")):
             path.method = method
-            o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method)
+            o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, method,
+                                reorder_group=rg)
             if cp:
                 o = ocph.place(o, t, gbs, dp, sp, configs.CAPACITY, 2048)
             lay = None
@@ -188,7 +191,12 @@ def main():
             table = planner.StepTable(t["lens"].astype(np.int32), t["mods"].astype(np.int32),
                                       t["ids"], t["carry_seq"].astype(np.int32),
                                       t["n_carry_seqs"], np.asarray(t["chunk_off"], np.int32))
-            dtab = planner.DeviceTable(table, dev)
+            if meta:  # decentralized loaders: this rank's share + the metadata all-gather
+                dtab = planner.gather_table(table.shard(rank, world), dev, dist.group.WORLD)
+                assert np.array_equal(dtab.blob.cpu().numpy()[:table.blob().size], table.blob())
+                table = dtab.table
+            else:
+                dtab = planner.DeviceTable(table, dev)
             plan = path.plan(dtab)
             plan.check(table)
             path.zero_llm()

@@ -112,3 +112,49 @@ def test_push_protocol_gloo(world, mode):
     for p in procs:
         p.join(timeout=60)
     assert res == {r: True for r in range(world)}
+
+
+def _meta_worker(rank, world, port, cases, result_q):
+    """Decentralized loaders: each rank packs only its share of the step into a
+    metadata record; one all-gather (gloo here, NCCL on the GPUs) and the
+    record assembly rebuild the global table on every rank, so every rank's
+    plan equals the centralized one."""
+    from paper_2605_08962_b200 import planner
+    from tests.test_gpu_planner import to_table
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok = True
+    cap, capc = 1024, 32
+    for t, st in cases:
+        table = to_table(t)
+        rec = torch.from_numpy(table.shard(rank, world).record(cap, capc))
+        out = [torch.empty_like(rec) for _ in range(world)]
+        dist.all_gather(out, rec)
+        got = oplan.assemble_records([o.numpy() for o in out], cap, capc)
+        for k in ("lens", "mods", "ids", "carry_seq"):
+            ok &= np.array_equal(got[k], np.asarray(t[k]))
+        ok &= list(got["chunk_off"]) == list(t["chunk_off"])
+        ok &= got["n_carry_seqs"] == t["n_carry_seqs"]
+        a = oplan.plan_step(got, 16384, st["gbs"], st["dp"], world // st["dp"], world)
+        b = oplan.plan_step(t, 16384, st["gbs"], st["dp"], world // st["dp"], world)
+        ok &= _digest(a) == _digest(b)
+    result_q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_metadata_all_gather_gloo(world):
+    cases = [(t, dict(st, dp=1)) for name, st, t, _ in golden_steps()
+             if name in ("cfg5", "cfg4", "target1") and st["step"] < 2]
+    assert cases
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_meta_worker, args=(r, world, port, cases, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}

@@ -256,6 +256,7 @@ def test_streaming_pipeline_matches_list_form(cuda_device, overlap):
         def encoder(k, p, s):
             o = os_[len(recv)]
             recv.append([path.recv_view(g, int(o["recv_rows"][0, g])).clone() for g in range(2)])
+            path.llm_view().zero_()  # text rows stay zero, as in the oracle
             path.encode_standin(p, dtab_of[len(recv) - 1], s)
 
         def after(k, p, s):

@@ -20,7 +20,8 @@ def _ngpus():
 @pytest.mark.parametrize("config", ["cfg5", "cfg3", "cfg4", "cfg2 proj", "cfg2 proj staged",
                                     "cfg5 lssp", "cfg4 cp", "cfg4 cp lssp", "cfg5 overlap",
                                     "cfg3 overlap", "cfg2 proj lssp", "cfg2 proj overlap",
-                                    "cfg2 proj overlap full", "cfg5 overlap full"])
+                                    "cfg2 proj overlap full", "cfg5 overlap full", "cfg5 meta",
+                                    "cfg4 meta", "cfg5 rg2"])
 def test_push_exchange_bit_exact(config):
     n = _ngpus()
     if n < 2:

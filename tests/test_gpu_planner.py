@@ -432,3 +432,42 @@ def test_plan_at_the_sample_limit(cuda_device):
               ids=np.append(t["ids"], n), chunk_off=[0, 1500, 3000, n + 1])
     with pytest.raises(ValueError, match="4096"):
         device_plan(t2, 16384, 8, 8, 1, 8, 0, "lpt")
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_assemble_table_matches_oracle(cuda_device, world):
+    """mux_assemble_table (csrc/meta.cu) on the records of every rank's share
+    rebuilds the centralized step table bit for bit; its device plan equals
+    the oracle's (the decentralized metadata all-gather)."""
+    import torch
+    cap, capc = 2048, 64
+    n = 0
+    for name, st, t, _ in golden_steps():
+        if st["step"] > 1:
+            continue
+        table = to_table(t)
+        recs = np.stack([table.shard(r, world).record(cap, capc) for r in range(world)])
+        want = oplan.assemble_records(list(recs), cap, capc)
+        blob = torch.full((table.blob().size + 4,), -7, dtype=torch.int64, device="cuda")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        dev = torch.from_numpy(recs.reshape(-1)).cuda()
+        _lib_ = planner._lib
+        _lib_.check(_lib_.lib().mux_assemble_table(dev.data_ptr(), world, cap, capc,
+                                                   blob.data_ptr(), blob.numel(),
+                                                   err.data_ptr(),
+                                                   torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert int(err.item()) == 0
+        assert np.array_equal(blob.cpu().numpy()[:table.blob().size], table.blob())
+        for k in ("lens", "ids", "carry_seq"):
+            assert np.array_equal(want[k], np.asarray(t[k]))
+        n += 1
+    assert n >= 4
+    # world 1 through gather_table (no process group): the plan of the gathered table
+    for name, st, t, _ in golden_steps():
+        if st["world"] == 1 and st["step"] == 0:
+            dt = planner.gather_table(to_table(t), "cuda")
+            cfg = planner.make_cfg(dt.table, configs.CAPACITY, st["gbs"], 1, 1, 1)
+            plan = planner.plan_step(dt, cfg)
+            plan.check(dt.table)
+            assert_plan_equal(plan.host(), oracle_plan(t, st), t, 0)

@@ -99,7 +99,7 @@ def test_export_batch_matches_reference_bytes(tmp_path):
 def test_capi_exports_every_declared_symbol():
     from paper_2605_08962_b200 import _lib
     hdr = open(os.path.join(ROOT, "include", "mux_b200.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|void|const char\*|size_t)\s+(mux_\w+)\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|void|const char\*|size_t)\s+(mux_\w+)\(", hdr, re.M))
     assert declared, "no declarations parsed"
     L = _lib.lib()
     for name in declared:
