@@ -41,24 +41,43 @@ def main():
            for r in range(world) if r != rank]
     A, B, Cm = ranges(loc), ranges(rem), ranges(rem + loc)
 
-    def go(rg, stream, grid=0):
+    def go(rg, stream, grid=0, mode=0):
         d, sr, b, mx, n = rg
-        _lib.check(L.mux_copy_ranges(n, d.data_ptr(), sr.data_ptr(), b.data_ptr(), mx, grid, 0,
-                                     stream.cuda_stream))
+        if n == 0 or mx == 0:
+            return
+        _lib.check(L.mux_copy_ranges(n, d.data_ptr(), sr.data_ptr(), b.data_ptr(), mx, grid,
+                                     mode, stream.cuda_stream))
 
-    def both():
+    def fork(remote_fn, local_grid=888):
         ev = torch.cuda.Event()
         ev.record(s1)
         s2.wait_event(ev)
-        go(B, s2, 296)
-        go(A, s1, 888)
+        remote_fn()
+        go(A, s1, local_grid)
         ev2 = torch.cuda.Event()
         ev2.record(s2)
         s1.wait_event(ev2)
 
+    def both():
+        fork(lambda: go(B, s2, 296))
+
+    def both_tma(grid):
+        return lambda: fork(lambda: go(B, s2, grid, 1))
+
+    def both_ce():
+        def ce():
+            for (d, sr, n) in rem:
+                if n:
+                    _lib.check(L.mux_memcpy_async(d, sr, n, s2.cuda_stream))
+        fork(ce, 1184)
+
     out = {"world": world, "local_mib": lm, "remote_mib_per_peer": rm}
     for nm, fn in (("A_local", lambda: go(A, s1)), ("B_remote", lambda: go(B, s1)),
-                   ("C_mixed_one_launch", lambda: go(Cm, s1)), ("D_two_streams", both)):
+                   ("B_remote_tma", lambda: go(B, s1, 296, 1)),
+                   ("C_mixed_one_launch", lambda: go(Cm, s1)), ("D_two_streams", both),
+                   ("E_remote_tma148_local_sm", both_tma(148)),
+                   ("E_remote_tma296_local_sm", both_tma(296)),
+                   ("F_remote_copy_engine_local_sm", both_ce)):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
