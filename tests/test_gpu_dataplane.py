@@ -328,3 +328,29 @@ def test_streaming_pipeline_matches_list_form(cuda_device, overlap):
             for g in range(2):
                 assert torch.equal(got_recv[k][g], want_recv[k][g]), (calls, k, g)
             assert torch.equal(got_llm[k], want_llm[k]), (calls, k)
+
+
+def test_dispatch_reads_pinned_host_rows(cuda_device):
+    """The fused loader transfer (bench e2e `fused_loader`): the
+    dispatch kernel reads each sample's rows straight from pinned host memory
+    (UVA) into the receive windows — bit-exact against the oracle."""
+    from paper_2605_08962_b200.dataplane import MuxPath
+    for name, st, t, _ in golden_steps():
+        if name == "target1" and st["world"] == 1 and st["step"] == 1:
+            break
+    cap, gbs, d_in = configs.CAPACITY, st["gbs"], (588, 512)
+    o = oplan.plan_step(t, cap, gbs, 1, 1, 1, 1, "lpt")
+    host = [payload(max(int(o["arena_rows"][0, g]), 1), d_in[g], 40 + g).pin_memory()
+            for g in range(2)]
+    path = MuxPath(capacity=cap, gbs=gbs, dp=1, d_in=d_in, d_llm=64)
+    table = to_table(t)
+    plan = path.plan(planner.DeviceTable(table, "cuda"))
+    plan.check(table)
+    path.dispatch(plan, host)
+    torch.cuda.synchronize()
+    ar = [[a.view(torch.int16).numpy().view(np.uint16) for a in host]]
+    recv, _, _ = odp.run_world(o, t, 1, ar, d_in, (64, 64), 64)
+    for g in range(2):
+        n = int(o["recv_rows"][0, g])
+        got = path.recv_view(g, n).cpu().view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got, recv[0][g]), g
