@@ -620,8 +620,9 @@ def projector_backward_stage(path, dtabs, steps_idx, plans_info, dy, stream, ctx
     _, burst, _, _ = peaks()
     return {"ms": ms, "tflops": flops / (ms / 1e3) / 1e12, "peak": burst,
             "frac": flops / (ms / 1e3) / 1e12 / burst,
-            "what": "dX = G W (pair GEMM, W^T) + dW = G^T X with fused db (pair GEMM, MN-major) "
-                    "per encoder group, after the gradient return; frac of the burst bf16 peak",
+            "what": "dX = G W (pair GEMM, W^T) + dW = G^T X (pair GEMM, MN-major) + db per "
+                    "encoder group, after the gradient return (not timed here); frac of the "
+                    "burst bf16 peak",
             "rank": ctx["rank"]}
 
 

@@ -10,7 +10,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmuxb200.so")
+LIB_PATH = os.environ.get("MUX_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libmuxb200.so")  # env: A/B of two builds
 
 MUX_OK, MUX_ERR_CONFIG, MUX_ERR_PACKING, MUX_ERR_VALUE, MUX_ERR_CUDA, MUX_ERR_RUNTIME = range(6)
 MODE_PACK, MODE_STEP = 0, 1
@@ -125,6 +126,8 @@ def lib():
                 f"{LIB_PATH} is missing; build it with `python -m paper_2605_08962_b200.build`")
         h = C.CDLL(LIB_PATH)
         for name, res, args in _SIGS:
+            if os.environ.get("MUX_LIB_PATH") and not hasattr(h, name):
+                continue  # an older build under A/B: bind what it has
             fn = getattr(h, name)
             fn.restype = res
             fn.argtypes = args

@@ -23,15 +23,23 @@ db = torch.empty(N, dtype=torch.bfloat16, device="cuda")
 s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+rows = torch.randperm(M, device="cuda").to(torch.int64)  # gathered variants: G = dY[rows]
+gathered = hasattr(L, "mux_proj_backward_rows")
+
+
 def run(which):
-    _lib.check(L.mux_proj_backward(G.data_ptr(), X.data_ptr(), W.data_ptr(), M, None, K, N,
-                                   dx.data_ptr() if "x" in which else None,
-                                   dw.data_ptr() if "w" in which else None,
-                                   db.data_ptr() if "w" in which and "n" not in which else None,
-                                   ws.data_ptr(), ws.numel(), 0, s))
+    ptrs = (dx.data_ptr() if "x" in which else None, dw.data_ptr() if "w" in which else None,
+            db.data_ptr() if "w" in which and "n" not in which else None)
+    if "g" in which:
+        _lib.check(L.mux_proj_backward_rows(G.data_ptr(), M, rows.data_ptr(), X.data_ptr(),
+                                            W.data_ptr(), M, None, K, N, *ptrs, ws.data_ptr(),
+                                            ws.numel(), 0, s))
+    else:
+        _lib.check(L.mux_proj_backward(G.data_ptr(), X.data_ptr(), W.data_ptr(), M, None, K, N,
+                                       *ptrs, ws.data_ptr(), ws.numel(), 0, s))
 
 
-for which in ("x", "w", "wn", "xw"):
+for which in ("x", "w", "wn", "xw") + (("xg", "wng", "wg", "xwg") if gathered else ()):
     for _ in range(3):
         run(which)
     torch.cuda.synchronize()
@@ -42,5 +50,5 @@ for which in ("x", "w", "wn", "xw"):
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
-    fl = 2.0 * M * K * N * len(which.replace("n", ""))
+    fl = 2.0 * M * K * N * len(which.replace("n", "").replace("g", ""))
     print(f"{which}: {ms:.4f} ms  {fl / ms / 1e9:.1f} TFLOP/s", flush=True)

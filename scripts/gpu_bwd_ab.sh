@@ -1,4 +1,6 @@
-# projector backward: probe timing + the backward tests
+# projector backward A/B: the pre-gather build (build/ab/lib_head.so) vs the current one
 python -m paper_2605_08962_b200.build > gpurun_out/build.log 2>&1 || exit 1
-python scripts/bwd_probe.py
-timeout 600 python -m pytest tests -q -m gpu -k "bwd or assemble" 2>&1 | tail -3
+for i in 1 2; do
+  echo "--- head"; MUX_LIB_PATH=build/ab/lib_head.so python scripts/bwd_probe.py
+  echo "--- new"; python scripts/bwd_probe.py
+done
