@@ -78,6 +78,21 @@ def parse():
 # workload
 # ----------------------------------------------------------------------------
 
+def balance_summary(plans_info, steps_idx):
+    """Balance diagnostics per step: encoder rows per rank before
+    the reorder (by origin rank) and after it (by encoder rank), and max/mean
+    imbalance ratios, averaged over the timed steps (first step's vectors kept)."""
+    def imb(v):
+        v = np.asarray(v, np.float64)
+        return float(v.max() / v.mean()) if v.size and v.mean() > 0 else 1.0
+    first = plans_info[steps_idx[0]]
+    return {"pre_loads_first_step": first["pre"].tolist(),
+            "post_loads_first_step": first["post"].tolist(),
+            "pre_imbalance": float(np.mean([imb(plans_info[i]["pre"]) for i in steps_idx])),
+            "post_imbalance": float(np.mean([imb(plans_info[i]["post"]) for i in steps_idx])),
+            "unit": "encoder rows (modality tokens) per rank; imbalance = max / mean"}
+
+
 def exchange_summary(plans_info, steps_idx, rank):
     """Rank-local bytes per step of the two exchanges and the share leaving the
     GPU over NVLink (the rest is a local HBM copy)."""
@@ -352,6 +367,8 @@ def measure(name, args, ctx, primary=True):
         for (_s, _d, rows, g, r) in info["dseg"]:
             disp_to[int(r)] += int(rows) * 2 * d_in[int(g)]
         m_tokens = int(info["recv_rows"].sum())  # modality tokens of the whole batch
+        pre = info["arena_rows"].sum(1).astype(np.float64)   # rows per origin (loader) rank
+        post = info["recv_rows"].sum(1).astype(np.float64)   # rows per encoder rank
         plans_info.append(dict(M=m_tokens, T=int(info["llm_rows"].sum()),
                                S=int(h[_lib.H_N_BATCH]),
                                recv=(int(h[_lib.H_RECV_ROWS0]), int(h[_lib.H_RECV_ROWS1])),
@@ -359,7 +376,7 @@ def measure(name, args, ctx, primary=True):
                                ret_bytes=int(h[_lib.H_RETURN_BYTES]),
                                disp_remote=int(h[_lib.H_DISPATCH_REMOTE]),
                                ret_remote=int(h[_lib.H_RETURN_REMOTE]),
-                               ret_to=ret_to, disp_to=disp_to))
+                               ret_to=ret_to, disp_to=disp_to, pre=pre, post=post))
     text_tokens, text_table = [], None
     if args.text_embed:  # synthetic token ids per distinct step, a 32K-row embedding table
         text_table = torch.randn(32000, d_llm, device=dev).to(torch.bfloat16)
@@ -571,6 +588,7 @@ def measure(name, args, ctx, primary=True):
             "launch": "one CUDA graph per step" if graphs is not None else "eager"},
         "roofline": roof,
         "exchange": exchange_summary(plans_info, steps_idx, rank),
+        "balance": balance_summary(plans_info, steps_idx),
         "stages": stages,
         "backward": backward,
         "gpu_launches": launches * args.steps,

@@ -61,3 +61,13 @@ def test_both_arms_print_the_same_config():
     a = bench.config_dict("cfg2", 1, n, 43355.0, 55499.25)
     b = bench.config_dict("cfg2", 1, n, 43355.0, 55499.25)
     assert a == b and a["workload"] == "cfg2" and a["global_batch"] == 4
+
+
+def test_balance_summary():
+    import numpy as np
+    info = [dict(pre=np.array([10.0, 2.0]), post=np.array([6.0, 6.0])),
+            dict(pre=np.array([4.0, 4.0]), post=np.array([5.0, 3.0]))]
+    b = bench.balance_summary(info, [0, 1])
+    assert b["pre_loads_first_step"] == [10.0, 2.0]
+    assert b["pre_imbalance"] == pytest.approx((10 / 6 + 1) / 2)
+    assert b["post_imbalance"] == pytest.approx((1 + 5 / 4) / 2)
