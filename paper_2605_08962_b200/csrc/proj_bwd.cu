@@ -169,15 +169,10 @@ __global__ void __launch_bounds__(kThreads, 1) dw_pair_kernel(const __grid_const
           if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
           const uint32_t bar = smem_u32(&full[stage]) & kPeerBitMask;
           const int m0 = kb * BK;
-#if MUX_BWD_TMA3D  // one 3D box {64 cols, 64 rows, 2 column blocks} per operand half
-          tma_load_3d_pair(sa, &P.tg, bar, 0, m0, n0 / 64, pol);
-          tma_load_3d_pair(sa + HALF_BYTES, &P.tx, bar, 0, m0, k0 / 64, pol);
-#else
           tma_load_2d_pair(sa, &P.tg, bar, n0, m0, pol);
           tma_load_2d_pair(sa + HALF_BYTES / 2, &P.tg, bar, n0 + 64, m0, pol);
           tma_load_2d_pair(sa + HALF_BYTES, &P.tx, bar, k0, m0, pol);
           tma_load_2d_pair(sa + HALF_BYTES + HALF_BYTES / 2, &P.tx, bar, k0 + 64, m0, pol);
-#endif
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -414,10 +409,6 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-#ifndef MUX_BWD_TMA3D
-#define MUX_BWD_TMA3D 0
-#endif
-
 static int make_map(CUtensorMap* m, const void* base, int64_t rows, int cols) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
@@ -432,15 +423,6 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int cols) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return MUX_ERR_CUDA;
   }
-#if MUX_BWD_TMA3D
-  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)cols / 64};
-  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, 128};
-  cuuint32_t box[3] = {64, BK, 2};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-#else
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
   cuuint32_t box[2] = {64, BK};
@@ -448,7 +430,6 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int cols) {
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-#endif
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
     return MUX_ERR_CUDA;
