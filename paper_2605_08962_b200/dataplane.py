@@ -273,7 +273,7 @@ class MuxPath:
         """Plan `dtab` into ring slot `slot` (0..RING-1) on the side stream.  `after`: an
         event the plan must follow (e.g. the step-table upload)."""
         self._ensure_ring()
-        self.gemm_ctas = self.num_sms - 1
+        self.gemm_ctas = self._pipelined_gemm_ctas()
         side = self._side
         if self._freed[slot] is not None:
             side.wait_event(self._freed[slot])
@@ -289,6 +289,13 @@ class MuxPath:
             self._row_map(p, self._row_ring[slot], side)
         self._ready[slot].record(side)
         return p
+
+    def _pipelined_gemm_ctas(self) -> int:
+        """GEMM CTAs while the next step's plan runs beside it: all SMs when the
+        planner's CTA fits next to a GEMM CTA (small step tables: its shared
+        memory is a few KB), else one SM left free for it (MUX_GEMM_ALL_SMS)."""
+        return self.num_sms if os.environ.get("MUX_GEMM_ALL_SMS", "0") == "1" \
+            else self.num_sms - 1
 
     def run_pipeline(self, steps=None, *, n=None, prepare=None, encoder=None, after_step=None,
                      kernel_events=None, start_event=None, stream=None):
@@ -736,7 +743,7 @@ class StepGraphs:
         if n % 2:
             raise ValueError("capture an even number of distinct steps (two plan buffers)")
         path._ensure_ring()
-        path.gemm_ctas = path.num_sms - 1
+        path.gemm_ctas = path._pipelined_gemm_ctas()
         dev = path.device
         self.path, self.n = path, n
         cfgs = [path.cfg_for(d.table) for d in dtabs]
