@@ -716,6 +716,8 @@ def nvlink_probe(path, ctx, nbytes=256 << 20, iters=5):
     world, rank, dev = ctx["world"], ctx["rank"], ctx["dev"]
     win = path.recv[0]
     nbytes = min(nbytes, win.tensor.numel()) & ~((1 << 20) - 1)
+    if nbytes == 0:  # a window too small to probe: fall back to the nominal figure
+        return {"bytes": 0, "peak_gbs": 900.0, "peak_source": "nominal (window too small to probe)"}
     src = torch.empty(nbytes, dtype=torch.uint8, device=dev).fill_(rank)
     dst = win.ptrs[(rank + 1) % world]
     L = _lib.lib()

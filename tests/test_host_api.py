@@ -155,3 +155,18 @@ def test_header_is_plain_c99(tmp_path):
     assert out.returncode == 0, out.stderr
     assert [int(x) for x in out.stdout.split()] == [
         C.sizeof(_lib.PlanCfg), C.sizeof(_lib.PlanLayout), C.sizeof(_lib.ProjGroup)]
+
+
+def test_integration_stub_mirrors_the_abi():
+    """The ctypes stub printed in INTEGRATION.md §2 (what the reference package
+    would add) mirrors mux_plan_cfg / mux_plan_layout of this build."""
+    import ctypes as C
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = next(b.split("```", 1)[0] for b in text.split("```python")[1:] if "class PlanCfg" in b)
+    body = code[code.index("class PlanCfg"):code.index("def hybrid_pack")]
+    ns = {"ctypes": C}
+    exec(body, ns)
+    out = (C.c_int64 * 3)()
+    _lib.lib().mux_abi_sizes(out)
+    assert C.sizeof(ns["PlanCfg"]) == out[0]
+    assert C.sizeof(ns["PlanLayout"]) == out[1]
