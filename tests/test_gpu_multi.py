@@ -35,3 +35,18 @@ def test_push_exchange_bit_exact(config):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
+
+
+def test_failure_path_poisons_every_rank():
+    """A rank that never dispatches: the others' waits time out, their poisoned
+    copies pass the poison on, every rank raises (tests/mgpu_poison_worker.py)."""
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29612",
+           os.path.join(ROOT, "tests", "mgpu_poison_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
