@@ -236,11 +236,11 @@ def test_grouped_reorder_and_restore(cuda_device):
     assert balance.zero_redundancy_filter(None, 1, 4, 16) == [1, 5, 9, 13]
 
 
-def lssp_device_plan(t, cap, gbs, dp, sp, world, me, method, sp_enc, eta):
+def lssp_device_plan(t, cap, gbs, dp, sp, world, me, method, sp_enc, eta, reorder_group=0):
     table = to_table(t)
     cfg = planner.make_cfg(table, cap, gbs, dp, sp, world, 1, method, False, me,
                            row_bytes_in=(1176, 1024), row_bytes_ret=(8192, 8192),
-                           lssp_sp=sp_enc, lssp_eta=eta)
+                           lssp_sp=sp_enc, lssp_eta=eta, reorder_group=reorder_group)
     plan = planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
     plan.check(table)
     return plan.host()
@@ -471,3 +471,24 @@ def test_assemble_table_matches_oracle(cuda_device, world):
             plan = planner.plan_step(dt, cfg)
             plan.check(dt.table)
             assert_plan_equal(plan.host(), oracle_plan(t, st), t, 0)
+
+
+@pytest.mark.parametrize("rg,sp_enc", [(4, 2), (4, 4), (2, 2), (8, 4)])
+def test_lssp_inside_reorder_groups_matches_oracle(cuda_device, rg, sp_enc):
+    """LSSP groups nested in reorder groups (the planner requires rg % sp_enc == 0):
+    every rank's LSSP layout and segment tables bit-exact against the oracle."""
+    from oracle import lssp as olssp
+    n = 0
+    for name, st, t, _ in golden_steps():
+        world, dp = st["world"], st["dp"]
+        if world < rg or world % rg:
+            continue
+        o = oplan.plan_step(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, 1,
+                            "lpt_local", reorder_group=rg)
+        lay = olssp.layout(o, t["lens"], world, 2048, sp_enc)
+        for me in range(world):
+            d = lssp_device_plan(t, configs.CAPACITY, st["gbs"], dp, world // dp, world, me,
+                                 "lpt_local", sp_enc, 2048, reorder_group=rg)
+            assert_lssp_equal(d, o, lay, t, me)
+            n += 1
+    assert n >= 4
