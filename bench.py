@@ -360,9 +360,10 @@ def measure(name, args, ctx, primary=True):
         dtabs.append(dt)
         arenas.append(ar)
         # return bytes of this rank per destination rank (NVLink accounting)
-        ret_to = np.zeros(world)
-        for (_s, _d, rows, g, r) in info["rseg"]:
-            ret_to[int(r)] += int(rows) * 2 * path.d_ret[int(g)]
+        ret_to = np.zeros(world)  # bytes that cross to each rank: with the fused projector
+        for (_s, _d, rows, g, r) in info["rseg"]:  # the GEMM stores d_llm-wide rows
+            wide = d_llm if (projector and not path.staged) else path.d_ret[int(g)]
+            ret_to[int(r)] += int(rows) * 2 * wide
         disp_to = np.zeros(world)
         for (_s, _d, rows, g, r) in info["dseg"]:
             disp_to[int(r)] += int(rows) * 2 * d_in[int(g)]
@@ -543,6 +544,9 @@ def measure(name, args, ctx, primary=True):
     if world > 1:
         roof["nvlink"] = nvlink_roofline(path, plans_info, steps_idx, dom_avg_s,
                                          stages["pack_dispatch_ms"], ctx, projector)
+        roof["nvlink"]["hardware_counters"] = (
+            "none: ncu is single-GPU only and NVML's NVLink byte counters (fields 138-141, "
+            "202, 204) answer NOT_SUPPORTED on this pool (scripts/nvml_probe.py)")
     if world > 1 and not projector:  # the exchange is the bottleneck: NVLink is the bound
         roof["hbm_side"] = {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac")}
         nv = roof["nvlink"]
