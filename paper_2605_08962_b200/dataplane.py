@@ -715,14 +715,38 @@ class MuxPath:
 
     def _raise_status(self, code: int):
         raise RuntimeError(f"data path poisoned: {self._POISON_WHY.get(code, code)}; the "
-                           "exchange buffers of this and later steps are not valid (rebuild "
-                           "the MuxPath)")
+                           "exchange buffers of this and later steps are not valid (every "
+                           "rank calls reset_status() to recover)")
 
     def check_wait(self):
         """Synchronise and raise if the path is poisoned."""
         code = int(self.wait_err.item())
         if code:
             self._raise_status(code)
+
+    def reset_status(self):
+        """Collective recovery from a poisoned path (every rank calls it): drain
+        this GPU, clear the status word, every flag channel and epoch counter and
+        the copy counters, then barrier.  Buffers keep their (partial) contents;
+        the next step rewrites them."""
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=self.group)
+        self.wait_err.zero_()
+        for f in (self.flags, self.flags_d, self.flags_e):
+            f.tensor.zero_()
+        for e in (self.epoch_ctr, self.epoch_d, self.epoch_e):
+            e.zero_()
+        self.sync.zero_()
+        self._e_sent = 0
+        self._fuse_e = False
+        self._status_ev = None
+        if self._status_host is not None:
+            self._status_host.zero_()
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:  # every rank's flags are clear before anyone signals again
+            self.flags.handle.barrier()
 
     def poll_status(self):
         """Raise if an earlier run_pipeline's status copy has landed and shows a

@@ -8,7 +8,8 @@ path, and the poisoned return copies publish the poison bit — the last rank's
 return wait then ends poisoned too (status 2 if the poisoned flags arrive first,
 1 if its own timeout fires first).  Every rank must end with a raised
 RuntimeError from check_wait(), and a poisoned rank's own return rows stay
-unwritten.  Every wait is bounded; no kernel hangs."""
+unwritten.  Then every rank calls reset_status() and a third step runs healthy
+with step 0's results.  Every wait is bounded; no kernel hangs."""
 
 import os
 import sys
@@ -57,6 +58,7 @@ def main():
     path.return_scatter(plan)
     torch.cuda.synchronize()
     path.check_wait()
+    step0_llm = path.llm_view(int(o["llm_rows"][rank])).clone()
     dist.barrier()
     # step 1: the last rank skips its dispatch
     path.zero_llm()
@@ -84,6 +86,24 @@ def main():
         for (i, src, dst_rank, dst_row, k) in o["pieces"]:
             if int(o["enc"][i]) == rank and dst_rank == rank and k:
                 ok &= bool((llm[dst_row:dst_row + k] == 0).all())
+    # recovery: every rank resets its status and flags together; the next step is
+    # healthy again and its LLM rows match step 0's (same plan, same inputs)
+    ref = None
+    path.reset_status()
+    path.zero_llm()
+    torch.cuda.synchronize()
+    dist.barrier()
+    path.dispatch(plan, arenas)
+    path.encode_standin(plan, dtab)
+    path.return_scatter(plan)
+    torch.cuda.synchronize()
+    try:
+        path.check_wait()
+    except RuntimeError:
+        ok = False
+    n = int(o["llm_rows"][rank])
+    ref = step0_llm
+    ok &= torch.equal(path.llm_view(n), ref)
     print(f"rank {rank}: status {code} ok={ok}", flush=True)
     t_ok = torch.tensor([int(ok)], device=dev)
     dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
