@@ -691,6 +691,8 @@ def nvlink_roofline(path, plans_info, steps_idx, ret_s, disp_ms, ctx, projector)
         return {"remote_bytes_max_rank": b, "egress_bytes": eg.tolist(),
                 "ingress_bytes": ing.tolist(), "local_bytes": np.diag(Mx).tolist(),
                 "exchange_ms": t_ms, "gbs": gbs, "frac_of_peak": gbs / probe["peak_gbs"],
+                "frac_of_alltoall": gbs / probe["alltoall_gbs"] if probe.get("alltoall_gbs")
+                else None,
                 "frac_of_900": gbs / 900.0}
 
     out = {"return": rec(Rm, ret_ms),
@@ -721,19 +723,30 @@ def nvlink_probe(path, ctx, nbytes=256 << 20, iters=5):
     win = path.recv[0]
     nbytes = min(nbytes, win.tensor.numel()) & ~((1 << 20) - 1)
     if nbytes == 0:  # a window too small to probe: fall back to the nominal figure
-        return {"bytes": 0, "peak_gbs": 900.0, "peak_source": "nominal (window too small to probe)"}
+        return {"bytes": 0, "peak_gbs": 900.0, "alltoall_gbs": None,
+                "peak_source": "nominal (window too small to probe)"}
     src = torch.empty(nbytes, dtype=torch.uint8, device=dev).fill_(rank)
     dst = win.ptrs[(rank + 1) % world]
     L = _lib.lib()
     s = torch.cuda.current_stream()
+    # all-to-all: nbytes split over every peer, written concurrently by one launch,
+    # each source rank into its own slice of every peer's window
+    share = (min(nbytes // max(world - 1, 1), win.tensor.numel() // world)) & ~4095
+    peers = [r for r in range(world) if r != rank]
+    a2a = [torch.tensor(v, dtype=torch.int64, device=dev) for v in (
+        [win.ptrs[r] + rank * share for r in peers],
+        [src.data_ptr() + k * share for k in range(len(peers))], [share] * len(peers))]
     res = {}
-    for nm, fn in (("sm_push_ring", lambda: L.mux_copy_bytes(C.c_void_p(dst),
-                                                                C.c_void_p(src.data_ptr()),
-                                                                nbytes, 0, C.c_void_p(s.cuda_stream))),
-                   ("copy_engine_ring", lambda: L.mux_memcpy_async(C.c_void_p(dst),
-                                                                   C.c_void_p(src.data_ptr()),
-                                                                   nbytes,
-                                                                   C.c_void_p(s.cuda_stream)))):
+    for nm, fn, moved in (
+            ("sm_push_ring", lambda: L.mux_copy_bytes(C.c_void_p(dst), C.c_void_p(src.data_ptr()),
+                                                      nbytes, 0, C.c_void_p(s.cuda_stream)),
+             nbytes),
+            ("copy_engine_ring", lambda: L.mux_memcpy_async(C.c_void_p(dst),
+                                                            C.c_void_p(src.data_ptr()), nbytes,
+                                                            C.c_void_p(s.cuda_stream)), nbytes),
+            ("sm_push_alltoall", lambda: L.mux_copy_ranges(
+                len(peers), a2a[0].data_ptr(), a2a[1].data_ptr(), a2a[2].data_ptr(), share, 0, 0,
+                C.c_void_p(s.cuda_stream)), share * len(peers))):
         _lib.check(fn(), nm)
         torch.cuda.synchronize()
         dist.barrier()
@@ -745,12 +758,13 @@ def nvlink_probe(path, ctx, nbytes=256 << 20, iters=5):
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / iters], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        res[nm + "_gbs"] = nbytes / (float(t.item()) / 1e3) / 1e9
+        res[nm + "_gbs"] = moved / (float(t.item()) / 1e3) / 1e9
         dist.barrier()
     res["bytes"] = nbytes
     res["peak_gbs"] = max(res["sm_push_ring_gbs"], res["copy_engine_ring_gbs"])
     res["peak_source"] = ("measured in this run: best of SM-store ring push and copy-engine "
                           "ring push, 1 peer per rank, per direction")
+    res["alltoall_gbs"] = res["sm_push_alltoall_gbs"]
     return res
 
 

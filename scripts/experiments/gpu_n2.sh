@@ -5,5 +5,5 @@ import json
 d = json.loads(open("gpurun_out/n2.json").read().strip().splitlines()[-1])
 for nm, r in (("cfg2", d), ("cfg5", d["cfg5"])):
     nv = r["roofline"]["nvlink"]
-    print(nm, round(r["value"]/1e6, 2), round(r["ms_per_step"], 4), "ret gbs", round(nv["return"]["gbs"], 1), round(nv["return"]["frac_of_peak"], 3), "e2e", round(r["e2e"]["value"]/1e6, 2))
+    print(nm, round(r["value"]/1e6, 2), round(r["ms_per_step"], 4), "ret gbs", round(nv["return"]["gbs"], 1), round(nv["return"]["frac_of_peak"], 3), nv["return"]["frac_of_alltoall"], nv["probe"])
 PY
