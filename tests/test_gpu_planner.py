@@ -315,12 +315,14 @@ def test_lssp_rejects_bad_groups(cuda_device):
             planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
 
 
-def cp_device_plan(t, cap, gbs, dp, sp, world, me, method, thr, lssp_sp=0, eta=0):
+def cp_device_plan(t, cap, gbs, dp, sp, world, me, method, thr, lssp_sp=0, eta=0,
+                   reorder_group=0, cost=None):
     table = to_table(t)
     cfg = planner.make_cfg(table, cap, gbs, dp, sp, world, 1, method, False, me,
                            row_bytes_in=(1176, 1024), row_bytes_ret=(8192, 8192),
                            reshard="cp_hybrid", cp_threshold=thr or 0,
-                           lssp_sp=lssp_sp, lssp_eta=eta)
+                           lssp_sp=lssp_sp, lssp_eta=eta, reorder_group=reorder_group,
+                           cost=cost)
     plan = planner.plan_step(planner.DeviceTable(table, "cuda"), cfg)
     plan.check(table)
     return plan.host()
@@ -492,3 +494,26 @@ def test_lssp_inside_reorder_groups_matches_oracle(cuda_device, rg, sp_enc):
             assert_lssp_equal(d, o, lay, t, me)
             n += 1
     assert n >= 4
+
+
+def test_cp_hybrid_with_reorder_groups_and_flops_costs(cuda_device):
+    """CpHybrid LLM placement on top of an encoder plan balanced inside reorder
+    groups of 2 with the flops cost: every rank bit-exact against the oracle."""
+    from oracle import cphybrid as ocph
+    n = 0
+    for name, st, t, _ in golden_steps():
+        for world, dp in ((4, 1), (4, 2), (8, 2)):
+            sp = world // dp
+            gbs = st["gbs"] * dp // st["dp"] if st["gbs"] % st["dp"] == 0 else st["gbs"]
+            try:
+                o = oplan.plan_step(t, configs.CAPACITY, gbs, dp, sp, world, 1, "lpt_local",
+                                    reorder_group=2, cost=FLOPS)
+            except ValueError:
+                continue
+            c = ocph.place(o, t, gbs, dp, sp, configs.CAPACITY, 0)
+            for me in range(world):
+                d = cp_device_plan(t, configs.CAPACITY, gbs, dp, sp, world, me, "lpt_local", 0,
+                                   reorder_group=2, cost=FLOPS)
+                assert_cp_equal(d, c, t, me)
+                n += 1
+    assert n > 8
