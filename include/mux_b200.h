@@ -411,7 +411,8 @@ int mux_assemble_table(const int32_t* records, int32_t world, int32_t cap_rows, 
  * skip that product.  Rows [M, round_up(M, 64)) of G and X are zeroed.
  * tcgen05 CTA-pair GEMMs (MN-major operands for dW); K % 256 == 0,
  * N % 256 == 0.  workspace >= mux_proj_backward_workspace(K, N, num_sms)
- * bytes (W^T, split-K partials); num_sms = SMs the launches may use (0: all). */
+ * bytes (W^T, split-K partials; one call at a time per workspace — it is
+ * stream-ordered scratch); num_sms = SMs the launches may use (0: all). */
 size_t mux_proj_backward_workspace(int32_t K, int32_t N, int32_t num_sms);
 int mux_proj_backward(const uint16_t* G, const uint16_t* X, const uint16_t* W, int64_t M_max,
                       const int64_t* M_dev, int32_t K, int32_t N, uint16_t* dX, uint16_t* dW,
