@@ -15,7 +15,9 @@
 //   proj_scatter_kernel       one CTA per SM, M128 N256 K16, 4-stage ring of
 //                             A 128x64 + B 256x64 (128-byte swizzle)
 //   proj_scatter_pair_kernel  (default) CTA pairs, tcgen05.mma.cta_group::2
-//                             M256 N256 K16, 4-stage ring of half tiles (below)
+//                             M256 N256 K16, 6-stage ring of half tiles (below);
+//                             on one GPU a warp's 32 output rows leave by one TMA
+//                             tensor store when they are consecutive rows
 // Both handle up to two problems (encoder groups) per launch.
 
 #include <cuda.h>
@@ -49,6 +51,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // the output buffers; their tiles are enumerated group after group, so one
 // persistent launch covers the whole step.
 constexpr int kMaxGroups = 2;
+constexpr int kMaxOutMaps = 8;
 
 struct GroupParams {
   CUtensorMap ta[kMaxGroups];  // X_g [M_max_g, K_g]
@@ -73,6 +76,13 @@ struct GroupParams {
   // status word of the path (nullable): nonzero = poisoned step (segcopy.cu):
   // compute nothing, publish the epoch with kPoisonBit
   const int32_t* poison;
+  // TMA-store epilogue (pair kernel, MUX_EPI_TMA, one GPU): one tensor map per
+  // output base (box 64 x 32 rows, 128-byte swizzle = the staging layout); a
+  // warp's 32 rows go out in one store when they are consecutive rows of one
+  // base (a sample's rows are contiguous in its packed sequence, so nearly all
+  // are), else row by row as before
+  int epi_tma, n_out;
+  CUtensorMap tout[kMaxOutMaps];
 };
 
 __device__ __forceinline__ bool is_poisoned(const GroupParams& P) {
@@ -350,7 +360,11 @@ constexpr int BM2 = 256, STAGES2 = MUX_PAIR_STAGES;
 constexpr int A2_BYTES = 128 * BK * 2;
 constexpr int B2_BYTES = 128 * BK * 2;
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
-constexpr int kSmem2 = STAGES2 * STAGE2_BYTES + 256 + kStagingBytes + 1024;
+#ifndef MUX_EPI_TMA
+#define MUX_EPI_TMA 1
+#endif
+constexpr int kStage2Off = MUX_EPI_TMA ? 1024 : 256;  // staging after the barriers (1 KB-aligned for TMA)
+constexpr int kSmem2 = STAGES2 * STAGE2_BYTES + kStage2Off + kStagingBytes + 1024;
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -470,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp & 3, colgrp = (warp - 2) >> 2;
-    uint4* stage = reinterpret_cast<uint4*>(smem + STAGES2 * STAGE2_BYTES + 256) +
+    uint4* stage = reinterpret_cast<uint4*>(smem + STAGES2 * STAGE2_BYTES + kStage2Off) +
                    (warp - 2) * (32 * 8);
     const uint32_t tempty_leader[2] = {mapa(smem_u32(&tempty[0]), 0),
                                        mapa(smem_u32(&tempty[1]), 0)};
@@ -482,15 +496,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint16_t* bias = P.bias[g];
       const int64_t m = (int64_t)m_blk * BM2 + (int)rank * 128 + quarter * 32 + lane;
       char* my_dst = nullptr;
+      int64_t my_rd = -1;
       if (m < tm.M[g]) {
         const int64_t rd = P.row_dst[g] ? P.row_dst[g][m] : m;  // NULL: row m of base 0
+        my_rd = rd;
         my_dst = static_cast<char*>(P.out_bases[rd >> 40]) +
                  ((rd & kRowMask) * N + (int64_t)n_blk * BN + colgrp * 128) * 2;
       }
+#if MUX_EPI_TMA
+      // the warp's 32 rows are consecutive rows of one output base: one TMA store
+      const int64_t rd0 = __shfl_sync(MUX_FULL, my_rd, 0);
+      const bool tma_ok = P.epi_tma && (rd0 >> 40) < P.n_out &&
+                          __all_sync(MUX_FULL, my_rd >= 0 && my_rd == rd0 + lane);
+#endif
       mbar_wait_bounded(&tfull[acc], acc_phase, false);
       fence_after();
 #pragma unroll 1
       for (int sub = 0; sub < 2; ++sub) {
+#if MUX_EPI_TMA
+        if (lane == 0) bulk_wait_read();  // the last TMA store has read the staging rows
+        __syncwarp();
+#endif
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           uint32_t v[32];
@@ -514,6 +540,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage[lane * 8 + ((j * 4 + q) ^ (lane & 7))] =
                 make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         }
+#if MUX_EPI_TMA
+        if (tma_ok) {
+          fence_proxy_async_smem();  // the staging writes, visible to the TMA engine
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&P.tout[rd0 >> 40], smem_u32(stage),
+                         n_blk * BN + colgrp * 128 + sub * 64, (int)(rd0 & kRowMask));
+            bulk_commit();
+          }
+          continue;
+        }
+#endif
         __syncwarp();
         const int c8 = lane & 7;
 #pragma unroll 4
@@ -534,6 +572,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+#if MUX_EPI_TMA
+  if (warp >= 2 && lane == 0) {
+    bulk_wait_all();  // every TMA store of this warp has completed
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+#endif
   fence_before();
   if (P.world > 0) __threadfence_system();
   __syncthreads();
@@ -578,6 +622,27 @@ static EncodeTiledFn encode_fn() {
       fn = reinterpret_cast<EncodeTiledFn>(p);
   }
   return fn;
+}
+
+static int make_map_box(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_cols,
+                        int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return MUX_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (output) failed (%d)", (int)r);
+    return MUX_ERR_CUDA;
+  }
+  return MUX_OK;
 }
 
 static int make_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows) {
@@ -687,6 +752,42 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
     }
     return world > 0 ? mux_signal(me, world, flags_peers, epoch_ctr, stream) : MUX_OK;
   }
+#if MUX_EPI_TMA
+  {
+    // output tensor maps, cached per (out_bases, N): the base pointers are read back
+    // once (they are per-path constants in dataplane.py)
+    struct OutMaps {
+      const void* key;
+      int N, n;
+      CUtensorMap m[kMaxOutMaps];
+    };
+    static OutMaps cache[8];
+    static int n_cache = 0;
+    // one GPU only: TMA stores into NVLink-peer memory are not used (not validated)
+    const int nb = world > 0 ? world : 1;
+    OutMaps* hit = nullptr;
+    for (int c = 0; c < n_cache; ++c)
+      if (cache[c].key == (const void*)out_bases && cache[c].N == N) hit = &cache[c];
+    if (!hit && world <= 0 && nb <= kMaxOutMaps) {
+      void* hb[kMaxOutMaps];
+      MUX_CUDA(cudaMemcpy(hb, out_bases, nb * sizeof(void*), cudaMemcpyDeviceToHost));
+      OutMaps& o = cache[n_cache < 8 ? n_cache++ : 7];
+      o.key = out_bases;
+      o.N = N;
+      o.n = nb;
+      for (int r = 0; r < nb; ++r) {
+        int st = make_map_box(&o.m[r], hb[r], 1ll << 30, N, 64, 32);
+        if (st) return st;
+      }
+      hit = &o;
+    }
+    if (hit) {
+      P.epi_tma = 1;
+      P.n_out = hit->n;
+      for (int r = 0; r < hit->n; ++r) P.tout[r] = hit->m[r];
+    }
+  }
+#endif
   static int pair = -1;  // the CTA-pair (cta_group::2) kernel unless MUX_GEMM_2CTA=0
   if (pair < 0) {
     const char* e = getenv("MUX_GEMM_2CTA");

@@ -80,6 +80,13 @@ __device__ __forceinline__ void bulk_store(void* gdst, uint32_t ssrc, uint32_t b
                "r"(ssrc), "r"(bytes)
                : "memory");
 }
+// TMA tensor store of a box from this CTA's shared memory (tile mode).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, uint32_t ssrc, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   m),
+               "r"(ssrc), "r"(x), "r"(y)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
