@@ -16,8 +16,8 @@
 //                             A 128x64 + B 256x64 (128-byte swizzle)
 //   proj_scatter_pair_kernel  (default) CTA pairs, tcgen05.mma.cta_group::2
 //                             M256 N256 K16, 6-stage ring of half tiles (below);
-//                             on one GPU a warp's 32 output rows leave by one TMA
-//                             tensor store when they are consecutive rows
+//                             a warp's 32 output rows leave by one TMA tensor
+//                             store when they are consecutive rows (local or peer)
 // Both handle up to two problems (encoder groups) per launch.
 
 #include <cuda.h>
@@ -76,11 +76,11 @@ struct GroupParams {
   // status word of the path (nullable): nonzero = poisoned step (segcopy.cu):
   // compute nothing, publish the epoch with kPoisonBit
   const int32_t* poison;
-  // TMA-store epilogue (pair kernel, MUX_EPI_TMA, one GPU): one tensor map per
-  // output base (box 64 x 32 rows, 128-byte swizzle = the staging layout); a
-  // warp's 32 rows go out in one store when they are consecutive rows of one
-  // base (a sample's rows are contiguous in its packed sequence, so nearly all
-  // are), else row by row as before
+  // TMA-store epilogue (pair kernel, MUX_EPI_TMA): one tensor map per output
+  // base, local or NVLink peer (box 64 x 32 rows, 128-byte swizzle = the staging
+  // layout); a warp's 32 rows go out in one store when they are consecutive rows
+  // of one base (a sample's rows are contiguous in its packed sequence, so nearly
+  // all are), else row by row as before
   int epi_tma, n_out;
   CUtensorMap tout[kMaxOutMaps];
 };
@@ -763,12 +763,20 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
     };
     static OutMaps cache[8];
     static int n_cache = 0;
-    // one GPU only: TMA stores into NVLink-peer memory are not used (not validated)
+    // across GPUs the maps cover the peers' LLM buffers too (TMA stores over
+    // NVLink); MUX_EPI_TMA_PEERS=0 keeps the register stores there
+    static int peers = -1;
+    if (peers < 0) {
+      const char* e = getenv("MUX_EPI_TMA_PEERS");
+      peers = e ? atoi(e) : 1;
+    }
     const int nb = world > 0 ? world : 1;
     OutMaps* hit = nullptr;
     for (int c = 0; c < n_cache; ++c)
       if (cache[c].key == (const void*)out_bases && cache[c].N == N) hit = &cache[c];
-    if (!hit && world <= 0 && nb <= kMaxOutMaps) {
+    if (world > 0 && !peers) {
+      // register stores across GPUs
+    } else if (!hit && nb <= kMaxOutMaps) {
       void* hb[kMaxOutMaps];
       MUX_CUDA(cudaMemcpy(hb, out_bases, nb * sizeof(void*), cudaMemcpyDeviceToHost));
       OutMaps& o = cache[n_cache < 8 ? n_cache++ : 7];
@@ -781,7 +789,7 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
       }
       hit = &o;
     }
-    if (hit) {
+    if (hit && (world <= 0 || peers)) {
       P.epi_tma = 1;
       P.n_out = hit->n;
       for (int r = 0; r < hit->n; ++r) P.tout[r] = hit->m[r];
