@@ -144,6 +144,8 @@ inline int lssp_of(const mux_plan_cfg& c) { return c.lssp_sp > 0 ? c.lssp_sp : 0
 inline int max_ret_of(const mux_plan_cfg& c) { return c.S * (c.sp + 1 + lssp_of(c)) + 1; }
 inline int max_disp_of(const mux_plan_cfg& c) { return c.S * (lssp_of(c) > 1 ? lssp_of(c) : 1); }
 constexpr int kDefaultChunkBytes = 32768;
+// proj_gemm.cu: host-known output bases of a device base array (TMA-store maps).
+int out_maps_set(void* const* out_bases_dev, int N, void* const* bases_host, int nb);
 // Completion-flag value bit marking a poisoned step (segcopy.cu failure path).
 constexpr uint64_t kPoisonBit = 1ull << 63;
 

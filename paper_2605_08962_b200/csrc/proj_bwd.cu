@@ -11,7 +11,8 @@
 //   dW = G^T . X      [N, K]   dw_pair_kernel below: reduction over the M rows,
 //                              both operands MN-major straight from G and X
 //   db = sum_m G[m,:] [N]      colsum_kernel (fp32 partials over 148 row ranges,
-//                              summed in order): one HBM pass over G.  A sum
+//                              summed in order): one HBM pass over G, on a side
+//                              stream beside the two GEMMs.  A sum
 //                              warp reading the staged G tiles inside
 //                              dw_pair_kernel was measured first: holding each
 //                              stage for it halved the GEMM (0.85 vs 0.38 ms)
@@ -507,11 +508,42 @@ extern "C" int mux_proj_backward(const uint16_t* G, const uint16_t* X, const uin
   // rows past the device count up to the next K-block must read as zero
   pad_rows_kernel<<<64, 256, 0, s>>>(const_cast<uint16_t*>(G), M_max, M_dev, N);
   pad_rows_kernel<<<64, 256, 0, s>>>(const_cast<uint16_t*>(X), M_max, M_dev, K);
+  // db runs on a side stream beside the GEMMs (an HBM pass next to two
+  // L2/tensor-bound kernels, whose CTAs leave room for it): fork here, join at
+  // the end; stream-ordered for the caller and capture-safe (events)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (db) {
+    static cudaStream_t s_side[16] = {};
+    static cudaEvent_t s_fork[16] = {}, s_join[16] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 16) dev = 0;
+    if (!s_side[dev]) {
+      MUX_CUDA(cudaStreamCreateWithFlags(&s_side[dev], cudaStreamNonBlocking));
+      MUX_CUDA(cudaEventCreateWithFlags(&s_fork[dev], cudaEventDisableTiming));
+      MUX_CUDA(cudaEventCreateWithFlags(&s_join[dev], cudaEventDisableTiming));
+    }
+    side = s_side[dev];
+    ev_fork = s_fork[dev];
+    ev_join = s_join[dev];
+    MUX_CUDA(cudaEventRecord(ev_fork, s));
+    MUX_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    float* part = reinterpret_cast<float*>(ws + L.colsum);
+    colsum_kernel<<<dim3((N / 8 + 255) / 256, kColsumSplits), 256, 0, side>>>(G, M_max, M_dev,
+                                                                              N, part);
+    colsum_reduce_kernel<<<(N + 255) / 256, 256, 0, side>>>(part, kColsumSplits, N, db);
+    MUX_CUDA(cudaGetLastError());
+    MUX_CUDA(cudaEventRecord(ev_join, side));
+  }
   MUX_CUDA(cudaGetLastError());
   if (dX) {  // dX = G . W: the forward pair GEMM with A = G and B = W^T
     wt_transpose_kernel<<<dim3(K / 64, N / 64), dim3(64, 8), 0, s>>>(W, Wt, N, K);
     set_ptr_kernel<<<1, 1, 0, s>>>(reinterpret_cast<void**>(ws + L.bases), dX);
     MUX_CUDA(cudaGetLastError());
+    void* host_base[1] = {dX};  // the maps of the TMA-store epilogue must see this dX
+    int mst = out_maps_set(reinterpret_cast<void* const*>(ws + L.bases), K, host_base, 1);
+    if (mst) return mst;
     mux_proj_group g{G, Wt, nullptr, M_max, M_dev, N, 0, nullptr};
     const int st = mux_proj_scatter_grouped(&g, 1, K, reinterpret_cast<void**>(ws + L.bases),
                                             2 * pairs, stream);
@@ -564,12 +596,6 @@ extern "C" int mux_proj_backward(const uint16_t* G, const uint16_t* X, const uin
       MUX_CUDA(cudaGetLastError());
     }
   }
-  if (db) {
-    float* part = reinterpret_cast<float*>(ws + L.colsum);
-    colsum_kernel<<<dim3((N / 8 + 255) / 256, kColsumSplits), 256, 0, s>>>(G, M_max, M_dev, N,
-                                                                           part);
-    colsum_reduce_kernel<<<(N + 255) / 256, 256, 0, s>>>(part, kColsumSplits, N, db);
-    MUX_CUDA(cudaGetLastError());
-  }
+  if (db) MUX_CUDA(cudaStreamWaitEvent(s, ev_join, 0));  // join the db side stream
   return MUX_OK;
 }

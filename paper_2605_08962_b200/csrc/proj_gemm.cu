@@ -83,6 +83,7 @@ struct GroupParams {
   // all are), else row by row as before
   int epi_tma, n_out;
   CUtensorMap tout[kMaxOutMaps];
+  const void* tout_base[kMaxOutMaps];  // the base each map was built for
 };
 
 __device__ __forceinline__ bool is_poisoned(const GroupParams& P) {
@@ -507,7 +508,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the warp's 32 rows are consecutive rows of one output base: one TMA store
       const int64_t rd0 = __shfl_sync(MUX_FULL, my_rd, 0);
       const bool tma_ok = P.epi_tma && (rd0 >> 40) < P.n_out &&
-                          __all_sync(MUX_FULL, my_rd >= 0 && my_rd == rd0 + lane);
+                          __all_sync(MUX_FULL, my_rd >= 0 && my_rd == rd0 + lane) &&
+                          P.out_bases[rd0 >> 40] == P.tout_base[rd0 >> 40];
 #endif
       mbar_wait_bounded(&tfull[acc], acc_phase, false);
       fence_after();
@@ -645,6 +647,76 @@ static int make_map_box(CUtensorMap* m, const void* base, int64_t rows, int cols
   return MUX_OK;
 }
 
+// Output tensor maps of the TMA-store epilogue, cached per device base array
+// (out_bases) and N.  The kernel uses a map only while out_bases[r] still equals
+// the base the map was built for (tout_base), so a stale entry falls back to the
+// row stores instead of writing elsewhere; out_maps_set refreshes an entry from
+// host-known bases (the projector backward's per-call dX).
+struct OutMaps {
+  const void* key;
+  int N, n;
+  const void* base[kMaxOutMaps];
+  CUtensorMap m[kMaxOutMaps];
+};
+static OutMaps g_out_maps[16];
+static int g_n_out_maps = 0;
+
+static int out_maps_build(OutMaps& o, const void* key, int N, void* const* bases, int nb) {
+  o.key = key;
+  o.N = N;
+  o.n = nb;
+  for (int r = 0; r < nb; ++r) {
+    o.base[r] = bases[r];
+    int st = make_map_box(&o.m[r], bases[r], 1ll << 30, N, 64, 32);
+    if (st) return st;
+  }
+  return MUX_OK;
+}
+
+static OutMaps* out_maps_find(const void* key, int N) {
+  for (int c = 0; c < g_n_out_maps; ++c)
+    if (g_out_maps[c].key == key && g_out_maps[c].N == N) return &g_out_maps[c];
+  return nullptr;
+}
+
+static OutMaps* out_maps_slot(const void* key, int N) {
+  OutMaps* o = out_maps_find(key, N);
+  if (o) return o;
+  return &g_out_maps[g_n_out_maps < 16 ? g_n_out_maps++ : 15];
+}
+
+// lookup, reading the base pointers back once for a new array
+static int out_maps_lookup(void* const* out_bases, int N, int nb, const OutMaps** out) {
+  OutMaps* o = out_maps_find(out_bases, N);
+  if (!o || o->n != nb) {
+    void* hb[kMaxOutMaps];
+    MUX_CUDA(cudaMemcpy(hb, out_bases, nb * sizeof(void*), cudaMemcpyDeviceToHost));
+    o = out_maps_slot(out_bases, N);
+    int st = out_maps_build(*o, out_bases, N, hb, nb);
+    if (st) return st;
+  }
+  *out = o;
+  return MUX_OK;
+}
+
+}  // namespace proj
+
+// host-known bases for a device base array (proj_bwd.cu: dX of this call)
+int out_maps_set(void* const* out_bases_dev, int N, void* const* bases_host, int nb) {
+  using namespace proj;
+  if (nb > kMaxOutMaps) return MUX_OK;
+  OutMaps* o = out_maps_find(out_bases_dev, N);
+  if (o && o->n == nb) {
+    bool same = true;
+    for (int r = 0; r < nb; ++r) same = same && o->base[r] == bases_host[r];
+    if (same) return MUX_OK;
+  }
+  o = out_maps_slot(out_bases_dev, N);
+  return out_maps_build(*o, out_bases_dev, N, bases_host, nb);
+}
+
+namespace proj {
+
 static int make_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) {
@@ -754,15 +826,6 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
   }
 #if MUX_EPI_TMA
   {
-    // output tensor maps, cached per (out_bases, N): the base pointers are read back
-    // once (they are per-path constants in dataplane.py)
-    struct OutMaps {
-      const void* key;
-      int N, n;
-      CUtensorMap m[kMaxOutMaps];
-    };
-    static OutMaps cache[8];
-    static int n_cache = 0;
     // across GPUs the maps cover the peers' LLM buffers too (TMA stores over
     // NVLink); MUX_EPI_TMA_PEERS=0 keeps the register stores there
     static int peers = -1;
@@ -771,28 +834,18 @@ extern "C" int mux_proj_scatter_grouped_signal(const mux_proj_group* groups, int
       peers = e ? atoi(e) : 1;
     }
     const int nb = world > 0 ? world : 1;
-    OutMaps* hit = nullptr;
-    for (int c = 0; c < n_cache; ++c)
-      if (cache[c].key == (const void*)out_bases && cache[c].N == N) hit = &cache[c];
-    if (world > 0 && !peers) {
-      // register stores across GPUs
-    } else if (!hit && nb <= kMaxOutMaps) {
-      void* hb[kMaxOutMaps];
-      MUX_CUDA(cudaMemcpy(hb, out_bases, nb * sizeof(void*), cudaMemcpyDeviceToHost));
-      OutMaps& o = cache[n_cache < 8 ? n_cache++ : 7];
-      o.key = out_bases;
-      o.N = N;
-      o.n = nb;
-      for (int r = 0; r < nb; ++r) {
-        int st = make_map_box(&o.m[r], hb[r], 1ll << 30, N, 64, 32);
-        if (st) return st;
-      }
-      hit = &o;
+    const OutMaps* hit = nullptr;
+    if ((world <= 0 || peers) && nb <= kMaxOutMaps) {
+      int st = out_maps_lookup(out_bases, N, nb, &hit);
+      if (st) return st;
     }
-    if (hit && (world <= 0 || peers)) {
+    if (hit) {
       P.epi_tma = 1;
       P.n_out = hit->n;
-      for (int r = 0; r < hit->n; ++r) P.tout[r] = hit->m[r];
+      for (int r = 0; r < hit->n; ++r) {
+        P.tout[r] = hit->m[r];
+        P.tout_base[r] = hit->base[r];
+      }
     }
   }
 #endif
