@@ -133,6 +133,8 @@ struct SegArgs {
   int32_t me, world;
   int32_t skip_rank;    // segments addressed to this rank are not copied (-1: none)
   int32_t grab;         // chunks per grab (0: adaptive)
+  int32_t tail_mult;    // multi-chunk grabs drop to one chunk for the last
+                        // tail_mult * grid * grab chunks (0: never)
   const int32_t* poison;  // status word: nonzero = step poisoned, copy nothing
 };
 
@@ -159,15 +161,27 @@ __global__ void __launch_bounds__(kCopyThreads) segcopy_kernel(SegArgs a, int sm
   // ~45 us tail (target-1: 0.171 -> 0.153 ms); kGrab for a cross-GPU exchange,
   // where consecutive chunks to one peer keep NVLink efficient (cfg5 at 4 GPUs:
   // 484 vs 438 M tok/s).  MUX_COPY_GRAB overrides.
+  // Near the end multi-chunk grabs shrink to one chunk, so the last CTAs do
+  // not leave a tail of up to `grab` chunks each (MUX_COPY_TAIL).
   const uint32_t grab = a.grab > 0 ? (uint32_t)a.grab : (a.flags_peers ? kGrab : 1u);
-  if (threadIdx.x == 0) s_grab[0] = atomicAdd(&a.sync[0], grab);
+  const int64_t tail = (int64_t)a.tail_mult * gridDim.x * grab;
+  __shared__ uint32_t s_n[2];
+  if (threadIdx.x == 0) {
+    s_n[0] = grab;
+    s_grab[0] = atomicAdd(&a.sync[0], grab);
+  }
   __syncthreads();
   auto c0 = [&](int s) -> int64_t { return staged ? s_c0[s] : a.chunk0[s]; };
   for (int buf = 0;; buf ^= 1) {
     const int64_t c_begin = s_grab[buf];
     if (c_begin >= nchunks) break;
-    if (threadIdx.x == 0) s_grab[buf ^ 1] = atomicAdd(&a.sync[0], grab);
-    const int64_t c_end = c_begin + grab < nchunks ? c_begin + grab : nchunks;
+    const uint32_t n_this = s_n[buf];
+    if (threadIdx.x == 0) {
+      const uint32_t gn = nchunks - c_begin <= tail ? 1u : grab;
+      s_n[buf ^ 1] = gn;
+      s_grab[buf ^ 1] = atomicAdd(&a.sync[0], gn);
+    }
+    const int64_t c_end = c_begin + n_this < nchunks ? c_begin + n_this : nchunks;
     int lo = 0, hi = nseg - 1;  // last segment with c0 <= c_begin
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -670,6 +684,14 @@ extern "C" int mux_segcopy_ex(const mux_plan_cfg* cfg, const void* plan, int32_t
     grab = e ? atoi(e) : 0;
   }
   a.grab = grab;
+  // MUX_COPY_TAIL (default 1, measured: cfg5 at 2 GPUs 294 vs 279 M tok/s; at 4
+  // GPUs 448-454 vs 448-457, 2 and 4 were slower there)
+  static int tail_mult = -1;
+  if (tail_mult < 0) {
+    const char* e = getenv("MUX_COPY_TAIL");
+    tail_mult = e ? atoi(e) : 1;
+  }
+  a.tail_mult = tail_mult;
   if (!sync || (flags_peers && !epoch_ctr)) {
     set_error("segment copy needs its sync counters (and an epoch counter to signal)");
     return MUX_ERR_VALUE;
