@@ -553,6 +553,9 @@ def measure(name, args, ctx, primary=True):
         roof.update(bound="nvlink", achieved=nv["return"]["gbs"], peak=nv["peak_gbs"],
                     unit="GB/s", frac=nv["return"]["frac_of_peak"],
                     peak_source=nv["peak_source"])
+        cb = nv["return"].get("combined_bound")
+        if cb:  # the same kernel against HBM and NVLink together (perfect overlap)
+            roof["frac_combined_hbm_nvlink"] = cb["frac"]
 
     # e2e: public API from pinned host buffers, H2D + D2H inside the timed region
     e2e = None
@@ -683,19 +686,37 @@ def nvlink_roofline(path, plans_info, steps_idx, ret_s, disp_ms, ctx, projector)
     ret_ms, disp_ms = gmax(ret_s * 1e3), gmax(disp_ms)
     probe = nvlink_probe(path, ctx)
 
-    def rec(Mx, t_ms):
+    def rec(Mx, t_ms, combined=False):
         off = Mx - np.diag(np.diag(Mx))
         eg, ing = off.sum(1), off.sum(0)
         b = float(max(eg.max(), ing.max()))
         gbs = b / (t_ms / 1e3) / 1e9 if t_ms > 0 else 0.0
-        return {"remote_bytes_max_rank": b, "egress_bytes": eg.tolist(),
-                "ingress_bytes": ing.tolist(), "local_bytes": np.diag(Mx).tolist(),
-                "exchange_ms": t_ms, "gbs": gbs, "frac_of_peak": gbs / probe["peak_gbs"],
-                "frac_of_alltoall": gbs / probe["alltoall_gbs"] if probe.get("alltoall_gbs")
-                else None,
-                "frac_of_900": gbs / 900.0}
+        r = {"remote_bytes_max_rank": b, "egress_bytes": eg.tolist(),
+             "ingress_bytes": ing.tolist(), "local_bytes": np.diag(Mx).tolist(),
+             "exchange_ms": t_ms, "gbs": gbs, "frac_of_peak": gbs / probe["peak_gbs"],
+             "frac_of_alltoall": gbs / probe["alltoall_gbs"] if probe.get("alltoall_gbs")
+             else None,
+             "frac_of_900": gbs / 900.0}
+        if combined and t_ms > 0:
+            # the copy moves local rows through HBM while it pushes remote rows:
+            # per rank, HBM bytes = local read+write + egress read + ingress write
+            # at the measured HBM copy rate, NVLink bytes = max(egress, ingress)
+            # at the measured all-to-all push rate; bound = the slower of the two
+            # (perfect overlap), max over ranks
+            hbm = peaks()[0]
+            link = probe.get("alltoall_gbs") or probe["peak_gbs"]
+            t_h = (2 * np.diag(Mx) + eg + ing) / (hbm * 1e9) * 1e3
+            t_l = np.maximum(eg, ing) / (link * 1e9) * 1e3
+            bound = float(np.max(np.maximum(t_h, t_l)))
+            r["combined_bound"] = {
+                "bound_ms": bound, "frac": bound / t_ms,
+                "hbm_ms_per_rank": t_h.tolist(), "nvlink_ms_per_rank": t_l.tolist(),
+                "hbm_gbs": hbm, "nvlink_gbs": link,
+                "model": "max over ranks of max(HBM bytes / measured HBM, NVLink bytes / "
+                         "measured all-to-all push); frac = bound / exchange_ms"}
+        return r
 
-    out = {"return": rec(Rm, ret_ms),
+    out = {"return": rec(Rm, ret_ms, combined=not projector),
            "dispatch": rec(Dm, disp_ms),
            "peak_gbs": probe["peak_gbs"],
            "peak_source": probe["peak_source"],
