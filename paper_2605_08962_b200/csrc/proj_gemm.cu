@@ -365,7 +365,13 @@ constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
 #define MUX_EPI_TMA 1
 #endif
 constexpr int kStage2Off = MUX_EPI_TMA ? 1024 : 256;  // staging after the barriers (1 KB-aligned for TMA)
-constexpr int kSmem2 = STAGES2 * STAGE2_BYTES + kStage2Off + kStagingBytes + 1024;
+// epilogue staging buffers per warp: 2 lets a sub-block's TMA store still read
+// one buffer while the next sub-block fills the other (needs a 5-stage ring)
+#ifndef MUX_EPI_BUFS
+#define MUX_EPI_BUFS 1
+#endif
+constexpr int kEpiBufs = MUX_EPI_BUFS;
+constexpr int kSmem2 = STAGES2 * STAGE2_BYTES + kStage2Off + kEpiBufs * kStagingBytes + 1024;
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -485,8 +491,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp & 3, colgrp = (warp - 2) >> 2;
-    uint4* stage = reinterpret_cast<uint4*>(smem + STAGES2 * STAGE2_BYTES + kStage2Off) +
-                   (warp - 2) * (32 * 8);
+    uint4* stage_w = reinterpret_cast<uint4*>(smem + STAGES2 * STAGE2_BYTES + kStage2Off) +
+                     (warp - 2) * (32 * 8 * kEpiBufs);
     const uint32_t tempty_leader[2] = {mapa(smem_u32(&tempty[0]), 0),
                                        mapa(smem_u32(&tempty[1]), 0)};
     int acc = 0;
@@ -515,8 +521,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_after();
 #pragma unroll 1
       for (int sub = 0; sub < 2; ++sub) {
+        uint4* stage = stage_w + (kEpiBufs == 2 ? sub * (32 * 8) : 0);
 #if MUX_EPI_TMA
-        if (lane == 0) bulk_wait_read();  // the last TMA store has read the staging rows
+        // the TMA store that last used this buffer has read it
+        if (lane == 0) bulk_wait_read_n<kEpiBufs - 1>();
         __syncwarp();
 #endif
 #pragma unroll
