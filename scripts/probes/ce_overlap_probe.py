@@ -8,6 +8,7 @@ alone.)  Under torchrun, every rank, max over ranks of CUDA-event time:
   local+sm  both SM copies concurrently (two streams)
   local+ce  SM local copy and copy-engine push concurrently (two streams)
   tma_push, local+tma[G]   the push by TMA bulk copies (mux_copy_ranges mode 1)
+  sm+ce_push, ce+ce_push   two R-byte pushes to the peer at once (aggregate link rate)
 
   torchrun --nproc-per-node 2 scripts/probes/ce_overlap_probe.py
 """
@@ -32,7 +33,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     L = _lib.lib()
     LB, RB = 160 << 20, 48 << 20
-    win = _Window(RB, dev, dist.group.WORLD, world)
+    win = _Window(2 * RB, dev, dist.group.WORLD, world)
     src_l = torch.empty(LB, dtype=torch.uint8, device=dev).fill_(1)
     dst_l = torch.empty(LB, dtype=torch.uint8, device=dev)
     src_r = torch.empty(RB, dtype=torch.uint8, device=dev).fill_(2)
@@ -52,8 +53,9 @@ def main():
         _lib.check(L.mux_copy_ranges(1, rng[0].data_ptr(), rng[1].data_ptr(), rng[2].data_ptr(),
                                      RB, grid, 1, s.cuda_stream))
 
-    def ce_push(s):
-        _lib.check(L.mux_memcpy_async(C.c_void_p(peer), src_r.data_ptr(), RB, s.cuda_stream))
+    def ce_push(s, off=0):
+        _lib.check(L.mux_memcpy_async(C.c_void_p(peer + off), src_r.data_ptr(), RB,
+                                      s.cuda_stream))
 
     cases = {
         "local": lambda: local(s1),
@@ -62,6 +64,8 @@ def main():
         "local+sm": lambda: (local(s1), sm_push(s2)),
         "local+sm148": lambda: (local(s1), sm_push(s2, 148)),
         "local+ce": lambda: (local(s1), ce_push(s2)),
+        "sm+ce_push": lambda: (sm_push(s1), ce_push(s2, RB)),  # 2 x RB to the peer
+        "ce+ce_push": lambda: (ce_push(s1), ce_push(s2, RB)),
         "tma_push": lambda: tma_push(s1),
         "local+tma": lambda: (local(s1), tma_push(s2)),
         "local+tma148": lambda: (local(s1), tma_push(s2, 148)),
