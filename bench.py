@@ -651,6 +651,31 @@ def projector_backward_stage(path, dtabs, steps_idx, plans_info, dy, stream, ctx
             "rank": ctx["rank"]}
 
 
+def combined_bound(per_step, hbm_gbs, link_gbs, t_ms):
+    """Roofline of an exchange copy that moves local rows through HBM while it
+    pushes remote rows over NVLink.  per_step: [step, sender, receiver] bytes.
+    Per rank: HBM bytes = local read + write + egress read + ingress write at
+    hbm_gbs; NVLink bytes = max(egress, ingress) at link_gbs.  A step's bound is
+    the slower of the two (perfect overlap) on its slowest rank; the bound is the
+    mean over the steps (the binding rank and term change from step to step),
+    and frac = bound / t_ms (the measured mean exchange time)."""
+    bounds, nv_bound = [], 0
+    for M in np.asarray(per_step, dtype=np.float64):
+        o = M - np.diag(np.diag(M))
+        e, i = o.sum(1), o.sum(0)
+        t_h = (2 * np.diag(M) + e + i) / (hbm_gbs * 1e9) * 1e3
+        t_l = np.maximum(e, i) / (link_gbs * 1e9) * 1e3
+        bounds.append(float(np.max(np.maximum(t_h, t_l))))
+        nv_bound += int(t_l.max() >= t_h.max())
+    bound = float(np.mean(bounds)) if bounds else 0.0
+    return {"bound_ms": bound, "frac": bound / t_ms if t_ms > 0 else None,
+            "bound_ms_per_step": bounds, "steps_nvlink_bound": nv_bound,
+            "hbm_gbs": hbm_gbs, "nvlink_gbs": link_gbs,
+            "model": "per timed step: max over ranks of max(HBM bytes / measured HBM, "
+                     "NVLink bytes / measured all-to-all push); bound = mean over steps; "
+                     "frac = bound / exchange_ms"}
+
+
 def nvlink_roofline(path, plans_info, steps_idx, ret_s, disp_ms, ctx, projector):
     """Per-GPU NVLink bandwidth of the two exchanges at N > 1.
 
@@ -700,30 +725,9 @@ def nvlink_roofline(path, plans_info, steps_idx, ret_s, disp_ms, ctx, projector)
              else None,
              "frac_of_900": gbs / 900.0}
         if per_step is not None and t_ms > 0:
-            # the copy moves local rows through HBM while it pushes remote rows:
-            # per rank, HBM bytes = local read+write + egress read + ingress write
-            # at the measured HBM copy rate, NVLink bytes = max(egress, ingress)
-            # at the measured all-to-all push rate; a step's bound = the slower
-            # of the two (perfect overlap) on its slowest rank; averaged over the
-            # timed steps (the binding rank and term change from step to step)
-            hbm = peaks()[0]
-            link = probe.get("alltoall_gbs") or probe["peak_gbs"]
-            bounds, nv_bound = [], 0
-            for M in per_step:
-                o = M - np.diag(np.diag(M))
-                e, i = o.sum(1), o.sum(0)
-                t_h = (2 * np.diag(M) + e + i) / (hbm * 1e9) * 1e3
-                t_l = np.maximum(e, i) / (link * 1e9) * 1e3
-                bounds.append(float(np.max(np.maximum(t_h, t_l))))
-                nv_bound += int(t_l.max() >= t_h.max())
-            bound = float(np.mean(bounds))
-            r["combined_bound"] = {
-                "bound_ms": bound, "frac": bound / t_ms,
-                "bound_ms_per_step": bounds, "steps_nvlink_bound": nv_bound,
-                "hbm_gbs": hbm, "nvlink_gbs": link,
-                "model": "per timed step: max over ranks of max(HBM bytes / measured HBM, "
-                         "NVLink bytes / measured all-to-all push); bound = mean over steps; "
-                         "frac = bound / exchange_ms"}
+            r["combined_bound"] = combined_bound(per_step, peaks()[0],
+                                                 probe.get("alltoall_gbs") or probe["peak_gbs"],
+                                                 t_ms)
         return r
 
     out = {"return": rec(Rm, ret_ms, per_step=None if projector else R_steps),

@@ -71,3 +71,24 @@ def test_balance_summary():
     assert b["pre_loads_first_step"] == [10.0, 2.0]
     assert b["pre_imbalance"] == pytest.approx((10 / 6 + 1) / 2)
     assert b["post_imbalance"] == pytest.approx((1 + 5 / 4) / 2)
+
+
+def test_combined_bound_per_step():
+    """The exchange roofline: per step the slower of HBM and NVLink on the
+    slowest rank, then the mean over steps (an NVLink-bound step is not hidden
+    by averaging the byte matrices first)."""
+    import numpy as np
+    MB = 1e6
+    # step 0: rank 1 pushes 70 MB to rank 0 (NVLink-bound); step 1: all local
+    s0 = np.array([[100 * MB, 0], [70 * MB, 60 * MB]])
+    s1 = np.array([[200 * MB, 0], [0, 200 * MB]])
+    r = bench.combined_bound([s0, s1], hbm_gbs=6500.0, link_gbs=700.0, t_ms=0.2)
+    b0 = max(70 * MB / 700e9, (2 * 100 * MB + 70 * MB) / 6500e9) * 1e3  # rank 0: ingress
+    b0 = max(b0, (2 * 60 * MB + 70 * MB) / 6500e9 * 1e3)
+    b1 = 2 * 200 * MB / 6500e9 * 1e3
+    assert r["bound_ms_per_step"] == pytest.approx([b0, b1])
+    assert r["bound_ms"] == pytest.approx((b0 + b1) / 2)
+    assert r["frac"] == pytest.approx((b0 + b1) / 2 / 0.2)
+    assert r["steps_nvlink_bound"] == 1
+    avg = bench.combined_bound([(s0 + s1) / 2], 6500.0, 700.0, 0.2)["bound_ms"]
+    assert avg < r["bound_ms"]  # averaging first understates the bound
