@@ -16,9 +16,8 @@ side stream and, with the default --pipeline 2, its dispatch on a copy stream
 under step k's projector/return; the timed region covers K whole steps.
 
 Weak scaling: every GPU owns `gbs_per_replica` sequences (dp = N).
-Rank 0 prints one JSON line.  Tuning switches (env): MUX_GEMM_2CTA,
-MUX_CHUNK_BYTES, MUX_COPY_GRID, MUX_DISPATCH_GRID, MUX_COPY_GRAB, MUX_FUSE_E,
-MUX_PROJECTOR_RETURN.
+Rank 0 prints one JSON line.  Tuning switches (env and build macros, with their
+defaults and measurements): DESIGN.md §11.
 """
 
 from __future__ import annotations
