@@ -337,8 +337,6 @@ def measure(name, args, ctx, primary=True):
                    lssp_sp=args.lssp_sp or world, reshard=args.reshard,
                    cp_threshold=args.cp_threshold, overlap_dispatch=args.pipeline >= 2,
                    text_embed=args.text_embed)
-    if args.pipeline >= 2 and "MUX_DISPATCH_GRID" not in os.environ:
-        path.dispatch_grid = -2 * path.num_sms  # lean copy CTAs beside the GEMM
     if projector:
         gen = torch.Generator(device=dev).manual_seed(77)
         for g in range(2):

@@ -166,7 +166,18 @@ class MuxPath:
         # copy work unit and grid of the segment copies (tuning knobs; 0 = default grid)
         self.chunk_bytes = int(os.environ.get("MUX_CHUNK_BYTES", "32768"))
         self.copy_grid = int(os.environ.get("MUX_COPY_GRID", "0"))
-        self.dispatch_grid = int(os.environ.get("MUX_DISPATCH_GRID", str(self.copy_grid)))
+        # an overlapped dispatch runs as lean copy CTAs (no shared memory) beside the
+        # return: 2 per SM next to the projector GEMM (its registers and shared
+        # memory leave room for no more), 3 per SM next to a return copy (a copy CTA
+        # holds 16K registers: 4 per SM would leave none for the return kernel,
+        # which then waits for the dispatch to drain)
+        env_dg = os.environ.get("MUX_DISPATCH_GRID")
+        if env_dg is not None:
+            self.dispatch_grid = int(env_dg)
+        elif overlap_dispatch:
+            self.dispatch_grid = -(2 if projector else 3) * self.num_sms
+        else:
+            self.dispatch_grid = self.copy_grid
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         # status word of the exchanges (the poison of segcopy.cu): a flag wait
         # that times out sets 1, one that sees a poisoned peer sets 2; later
