@@ -70,6 +70,19 @@ def test_dataplane_golden_steps_narrow(cuda_device):
     assert n >= 6
 
 
+def test_dataplane_sm_return_path(cuda_device):
+    """Return rows that are not 16-byte multiples (d_llm 20: 40 B) take the SM copy
+    at one GPU instead of the TMA-engine copy (segcopy.cu MUX_COPY_BULK rule); both
+    must give the same bits."""
+    n = 0
+    for name, st, t, _ in golden_steps():
+        if st["world"] != 1 or n >= 3:
+            continue
+        run_step(t, configs.CAPACITY, st["gbs"], (20, 8), 20)
+        n += 1
+    assert n == 3
+
+
 def test_dataplane_target1_full_width(cuda_device):
     """target-1 step 0 at the real widths: 588/512-wide loader rows, 4096-wide returns."""
     for name, st, t, _ in golden_steps():
