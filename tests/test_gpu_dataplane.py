@@ -71,16 +71,20 @@ def test_dataplane_golden_steps_narrow(cuda_device):
 
 
 def test_dataplane_sm_return_path(cuda_device):
-    """Return rows that are not 16-byte multiples (d_llm 20: 40 B) take the SM copy
-    at one GPU instead of the TMA-engine copy (segcopy.cu MUX_COPY_BULK rule); both
-    must give the same bits."""
-    n = 0
-    for name, st, t, _ in golden_steps():
-        if st["world"] != 1 or n >= 3:
-            continue
-        run_step(t, configs.CAPACITY, st["gbs"], (20, 8), 20)
-        n += 1
-    assert n == 3
+    """At one GPU the return and gradient copies default to the TMA engine
+    (segcopy.cu MUX_COPY_BULK); the SM copy they replaced must still give the
+    same bits: the golden-step and full-width cases again with MUX_COPY_BULK=0
+    (read once per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MUX_COPY_BULK="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        f"{__file__}::test_dataplane_golden_steps_narrow",
+                        f"{__file__}::test_dataplane_target1_full_width"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_dataplane_target1_full_width(cuda_device):
