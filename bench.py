@@ -963,28 +963,28 @@ def run_e2e_one(args, path, tables, arenas, plans_info, n_distinct, projector, d
     trace = None  # MUX_E2E_TRACE=1: per-step upload / step-end events to stderr
     counts = {"h2d": 0, "d2h": 0}
 
+    def mark(name, k, s):
+        if trace is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            trace.append((name, k, e, time.perf_counter()))
+
     def prepare(k):
         """Upload step k into input slot k % 2 (the loader side of the pipeline)."""
         i, slot = k % n_distinct, k % 2
         if consumed[slot] is not None:  # step k-2 is done with this slot
             up.wait_event(consumed[slot])
-        if trace is not None:
-            trace.append(("up", k, torch.cuda.Event(enable_timing=True), time.perf_counter()))
-            trace[-1][2].record(up)
+        mark("up", k, up)
         with torch.cuda.stream(up):
             blob = dev_tab[slot][: host_tabs[i].numel()]
             blob.copy_(host_tabs[i], non_blocking=True)
-            if trace is not None:
-                trace.append(("tab", k, torch.cuda.Event(enable_timing=True), time.perf_counter()))
-                trace[-1][2].record(up)
+            mark("tab", k, up)
             if not fused_loader:
                 for g in range(2):
                     n = host_ar[i][g].numel()
                     dev_ar[slot][g][:n].copy_(host_ar[i][g].view(-1), non_blocking=True)
         uploaded[slot].record(up)
-        if trace is not None:
-            trace.append(("up_end", k, torch.cuda.Event(enable_timing=True), time.perf_counter()))
-            trace[-1][2].record(up)
+        mark("up_end", k, up)
         counts["h2d"] += host_tabs[i].numel() * 8 + sum(b.numel() * 2 for b in host_ar[i])
         if fused_loader:  # the dispatch kernel reads the pinned rows over PCIe
             shaped = host_ar[i]
@@ -1001,9 +1001,7 @@ def run_e2e_one(args, path, tables, arenas, plans_info, n_distinct, projector, d
         if path.step_done is not None:
             s.wait_event(path.step_done)
         out_hdr[slot].copy_(p.view("header", _lib.H_SLOTS), non_blocking=True)
-        if trace is not None:
-            trace.append(("step_end", k, torch.cuda.Event(enable_timing=True), time.perf_counter()))
-            trace[-1][2].record(s)
+        mark("step_end", k, s)
         c = torch.cuda.Event()
         c.record(s)
         consumed[slot] = c
